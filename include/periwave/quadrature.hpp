@@ -1,0 +1,3 @@
+// Forwarding header: the whole drop-in API lives in periwave/periwave.hpp.
+#pragma once
+#include "periwave/periwave.hpp"

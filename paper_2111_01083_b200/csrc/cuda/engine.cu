@@ -1,0 +1,630 @@
+// Device plan (periodizer tables uploaded once per device) and the
+// orchestration of apply_far / total_field / accumulate on device memory.
+// Mirrors the control flow of /root/reference/proj/src/apply.cpp:417-556.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "engine.hpp"
+
+namespace pwb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void throw_internal(const char* what) { throw InternalFailure(what); }
+
+namespace {
+std::atomic<long> g_launches{0};
+}
+void count_launches(long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+DevBuf::~DevBuf() {
+  if (p_) cudaFree(p_);
+}
+
+void* DevBuf::ensure(size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (bytes > n_) {
+    if (p_) cuda_check(cudaFree(p_), "cudaFree");
+    p_ = nullptr;
+    n_ = 0;
+    cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
+    n_ = bytes;
+  }
+  return p_;
+}
+
+PinnedBuf::~PinnedBuf() {
+  if (p_) cudaFreeHost(p_);
+}
+
+void* PinnedBuf::ensure(size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (bytes > n_) {
+    if (p_) cuda_check(cudaFreeHost(p_), "cudaFreeHost");
+    p_ = nullptr;
+    n_ = 0;
+    cuda_check(cudaMallocHost(&p_, bytes), "cudaMallocHost");
+    n_ = bytes;
+  }
+  return p_;
+}
+
+using periwave::ErrorCode;
+using periwave::require;
+
+Kind kind_of(const periwave::Periodizer& pz) {  // apply.cpp:20-26
+  if (pz.multipole_order >= 1) return Kind::Multipole;
+  if (pz.pde == periwave::Pde::Stokes || pz.pde == periwave::Pde::ModStokes) return Kind::Velocity;
+  return Kind::Scalar;
+}
+
+ModeTable Family::table() const {
+  ModeTable t;
+  t.phase = static_cast<const double*>(phase.get());
+  t.decay_t = static_cast<const double*>(decay_t.get());
+  t.decay_s = static_cast<const double*>(decay_s.get());
+  t.shift_t = static_cast<const double*>(shift_t.get());
+  t.shift_s = static_cast<const double*>(shift_s.get());
+  t.axis = static_cast<const int*>(axis.get());
+  t.count = count;
+  return t;
+}
+
+namespace {
+
+template <class T>
+void upload(DevBuf& b, const std::vector<T>& v) {
+  T* p = b.as<T>(v.size());
+  if (!v.empty()) cuda_check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+}
+
+struct HostModes {
+  std::vector<double> phase, dt, ds, st, ss;
+  std::vector<int> axis;
+  void add(const periwave::ModeSet& m) {
+    for (size_t r = 0; r < m.size(); ++r) {
+      phase.push_back(m.phase[r]);
+      dt.push_back(m.decay_t[r]);
+      ds.push_back(m.decay_s[r]);
+      st.push_back(m.shift_t[r]);
+      ss.push_back(m.shift_s[r]);
+      axis.push_back(m.axis == periwave::Axis::Horizontal ? 1 : 0);
+    }
+  }
+  void to(Family& f) {
+    f.count = static_cast<int>(phase.size());
+    upload(f.phase, phase);
+    upload(f.decay_t, dt);
+    upload(f.decay_s, ds);
+    upload(f.shift_t, st);
+    upload(f.shift_s, ss);
+    upload(f.axis, axis);
+  }
+};
+
+void push_c(std::vector<double>& v, periwave::cplx c) {
+  v.push_back(c.real());
+  v.push_back(c.imag());
+}
+void push_m(std::vector<double>& v, const periwave::Mat2c& m) {
+  push_c(v, m.a11);
+  push_c(v, m.a12);
+  push_c(v, m.a21);
+  push_c(v, m.a22);
+}
+
+void require_vertical_m0(const periwave::ModeSet& m, bool has_m0) {
+  require(!has_m0 || m.axis == periwave::Axis::Vertical || m.size() == 0, ErrorCode::Unsupported,
+          "rank-one m0 terms are supported on vertical parts only");
+}
+
+__global__ void m0_kernel(const double* mom, int ia, int ib, double a00, double a01, double a10, double a11, int ko,
+                          double* out) {
+  if (threadIdx.x != 0) return;
+  const double u = mom[ia], v = mom[ib];
+  out[0] = a00 * u + a01 * v;
+  out[1] = 0.0;
+  if (ko == 2) {
+    out[2] = a10 * u + a11 * v;
+    out[3] = 0.0;
+  }
+}
+
+}  // namespace
+
+Plan::Plan(const periwave::Periodizer& pz, int device) : pz_(pz), device_(device) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_), "sm count");
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  build_families();
+  for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "event");
+  flag_.ensure(sizeof(int));
+  host_checks_.ensure(64 * sizeof(double));
+}
+
+Plan::~Plan() {
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Plan::phase_ms(double* far_ms, double* near_ms) {
+  float a = 0.f, b = 0.f;
+  if (far_timed_) cuda_check(cudaEventElapsedTime(&a, ev_[0], ev_[1]), "event time");
+  if (near_timed_) cuda_check(cudaEventElapsedTime(&b, ev_[2], ev_[3]), "event time");
+  *far_ms = far_timed_ ? a : 0.0;
+  *near_ms = near_timed_ ? b : 0.0;
+}
+
+void Plan::build_families() {
+  const Kind kind = kind_of(pz_);
+  if (kind != Kind::Velocity) {
+    auto f = std::make_unique<Family>();
+    f->kind = FamilyKind::Scalar;
+    f->ws = kind == Kind::Multipole ? WeightSet::Coef : WeightSet::Charge;
+    f->ko = 1;
+    HostModes hm;
+    std::vector<double> diag;
+    double m0sum = 0.0;
+    bool any_m0 = false;
+    for (const auto& p : pz_.scalar_parts) {
+      require(p.diag.size() == p.modes.size(), ErrorCode::LengthMismatch, "scalar part diag/mode size mismatch");
+      require_vertical_m0(p.modes, p.has_m0);
+      hm.add(p.modes);
+      for (const auto& c : p.diag) push_c(diag, c);
+      if (p.has_m0) {
+        any_m0 = true;
+        m0sum += p.m0_coef;
+      }
+    }
+    hm.to(*f);
+    upload(f->t[0], diag);
+    if (any_m0 && kind == Kind::Scalar) {
+      f->has_lin = true;
+      f->ia = 0;
+      f->ib = 0;
+      f->mlin[0] = m0sum;
+    }
+    fams_.push_back(std::move(f));
+    return;
+  }
+  if (!pz_.block_parts.empty()) {
+    auto f = std::make_unique<Family>();
+    f->kind = FamilyKind::Block;
+    f->ko = 2;
+    HostModes hm;
+    std::vector<double> da, db;
+    std::vector<int> tt;
+    bool any_three = false, any_m0 = false;
+    double msum[4] = {0, 0, 0, 0};
+    for (const auto& p : pz_.block_parts) {
+      require(p.diag_a.size() == p.modes.size(), ErrorCode::LengthMismatch, "block part diag/mode size mismatch");
+      require(!p.three_term || p.diag_b.size() == p.modes.size(), ErrorCode::LengthMismatch,
+              "block part diag_b size mismatch");
+      require_vertical_m0(p.modes, p.has_m0);
+      hm.add(p.modes);
+      for (size_t r = 0; r < p.modes.size(); ++r) {
+        push_m(da, p.diag_a[r]);
+        push_m(db, p.three_term ? p.diag_b[r] : periwave::Mat2c{});
+        tt.push_back(p.three_term ? 1 : 0);
+      }
+      any_three = any_three || p.three_term;
+      if (p.has_m0) {
+        any_m0 = true;
+        msum[0] += p.m0_mat.a11;
+        msum[1] += p.m0_mat.a12;
+        msum[2] += p.m0_mat.a21;
+        msum[3] += p.m0_mat.a22;
+      }
+    }
+    f->ws = any_three ? WeightSet::ForceW : WeightSet::Force;
+    hm.to(*f);
+    upload(f->t[0], da);
+    upload(f->t[1], db);
+    upload(f->three_term, tt);
+    if (any_m0) {
+      f->has_lin = true;
+      f->ia = 1;
+      f->ib = 2;
+      std::memcpy(f->mlin, msum, sizeof msum);
+    }
+    fams_.push_back(std::move(f));
+  }
+  if (!pz_.stresslet_parts.empty()) {
+    auto f = std::make_unique<Family>();
+    f->kind = FamilyKind::Stresslet;
+    f->ws = WeightSet::DoubleLayer;
+    f->ko = 2;
+    HostModes hm;
+    std::vector<double> a1, a2, sm, sa, sb, off;
+    double csum = 0.0;
+    bool any_m0 = false;
+    for (const auto& p : pz_.stresslet_parts) {
+      const size_t n = p.modes.size();
+      require(p.a1.size() == n && p.a2.size() == n && p.smat.size() == n && p.sa.size() == n && p.sb.size() == n &&
+                  p.off.size() == n,
+              ErrorCode::LengthMismatch, "stresslet part table size mismatch");
+      require_vertical_m0(p.modes, p.has_m0);
+      hm.add(p.modes);
+      for (size_t r = 0; r < n; ++r) {
+        push_m(a1, p.a1[r]);
+        push_m(a2, p.a2[r]);
+        push_m(sm, p.smat[r]);
+        push_c(sa, p.sa[r]);
+        push_c(sb, p.sb[r]);
+        push_c(off, p.off[r]);
+      }
+      if (p.has_m0) {
+        any_m0 = true;
+        csum += p.m0_coef;
+      }
+    }
+    hm.to(*f);
+    upload(f->t[0], a1);
+    upload(f->t[1], a2);
+    upload(f->t[2], sm);
+    upload(f->t[3], sa);
+    upload(f->t[4], sb);
+    upload(f->t[5], off);
+    if (any_m0) {
+      f->has_lin = true;
+      f->ia = 3;
+      f->ib = 4;
+      f->mlin[0] = csum;
+      f->mlin[3] = csum;
+    }
+    fams_.push_back(std::move(f));
+  }
+  if (!pz_.pressure_parts.empty()) {
+    auto f = std::make_unique<Family>();
+    f->kind = FamilyKind::Pressure;
+    f->ws = WeightSet::Force;
+    f->ko = 1;
+    f->pressure = true;
+    HostModes hm;
+    std::vector<double> diag, row;
+    bool any_m0 = false;
+    double cx = 0.0, cy = 0.0;
+    for (const auto& p : pz_.pressure_parts) {
+      require(p.diag.size() == p.modes.size() && p.row.size() == p.modes.size(), ErrorCode::LengthMismatch,
+              "pressure part table size mismatch");
+      require_vertical_m0(p.modes, p.has_m0);
+      hm.add(p.modes);
+      for (size_t r = 0; r < p.modes.size(); ++r) {
+        push_c(diag, p.diag[r]);
+        push_c(row, p.row[r].x);
+        push_c(row, p.row[r].y);
+      }
+      if (p.has_m0) {
+        any_m0 = true;
+        cx += p.m0_coef * p.m0_row.x;
+        cy += p.m0_coef * p.m0_row.y;
+      }
+    }
+    hm.to(*f);
+    upload(f->t[0], diag);
+    upload(f->t[1], row);
+    if (any_m0) {
+      f->has_cst = true;
+      f->ia = 1;
+      f->ib = 2;
+      f->mcst[0] = cx;
+      f->mcst[1] = cy;
+    }
+    fams_.push_back(std::move(f));
+  }
+}
+
+int Plan::s2pw_chunks(size_t ns, int modes, int k) const {
+  const int mt = k >= 8 ? 1 : 8 / k;
+  const int mode_blocks = std::max(1, (modes + mt - 1) / mt);
+  long want = (4L * sms_ + mode_blocks - 1) / mode_blocks;
+  const long by_src = static_cast<long>(std::max<size_t>(1, ns / 2048));
+  want = std::min(want, by_src);
+  return static_cast<int>(std::max(1L, std::min(want, 1024L)));
+}
+
+size_t Plan::coeff_size(const Opts& o) const {
+  size_t n = 0;
+  for (const auto& f : fams_) {
+    if (f->pressure && !o.with_pressure) continue;
+    n += static_cast<size_t>(f->count) * weight_count(f->ws) * 2;
+  }
+  return n + kMoments + 3;  // moments, padded to a multiple of 8 bytes * 8
+}
+
+void Plan::validate(const DevSys& s, const Opts& o, bool far_checks, bool neutrality) {
+  const Kind kind = kind_of(pz_);
+  // apply.cpp:350-364 + cell.cpp:84-91: the strength arrays the kind needs
+  if (kind == Kind::Multipole)
+    require(s.ns == 0 || s.coef, ErrorCode::LengthMismatch, "multipole apply requires one complex coefficient per source");
+  else if (pz_.dlp)
+    require(s.ns == 0 || (s.f && s.nrm), ErrorCode::LengthMismatch,
+            "double-layer apply requires a force vector and a unit normal per source");
+  else if (kind == Kind::Velocity)
+    require(s.ns == 0 || s.f, ErrorCode::LengthMismatch, "velocity apply requires one force vector per source");
+  else
+    require(s.ns == 0 || s.q, ErrorCode::LengthMismatch, "scalar apply requires one charge per source");
+  if (far_checks) {
+    require(!o.with_pressure || !pz_.pressure_parts.empty(), ErrorCode::Unsupported,
+            "pressure output is not available for this periodizer");
+  } else {
+    require(!o.with_pressure || kind == Kind::Velocity, ErrorCode::Unsupported,
+            "pressure output is not available for this periodizer");
+    require(!(o.with_pressure && pz_.dlp), ErrorCode::Unsupported,
+            "pressure output is not available for the double-layer kernel");
+  }
+  require(!o.with_gradient || (kind == Kind::Scalar && pz_.pde == periwave::Pde::ModHelmholtz), ErrorCode::Unsupported,
+          "gradient output is available for the modified Helmholtz scalar kernel");
+  cudaStream_t st = stream_for(o);
+  ReduceArgs ra;
+  ra.src = s.src;
+  ra.ns = s.ns;
+  ra.q = s.q;
+  ra.vec = s.f;
+  ra.coef = s.coef;
+  ra.nrm = s.nrm;
+  ra.tgt = far_checks ? s.tgt : nullptr;
+  ra.nt = far_checks ? s.nt : 0;
+  ra.d = pz_.cell.d;
+  ra.xi = pz_.cell.xi;
+  ra.eta = pz_.cell.eta;
+  double* bm = red_m_.as<double>(kReduceBlocks * kMoments);
+  double* bc = red_c_.as<double>(kReduceBlocks * kChecks);
+  double* outv = red_out_.as<double>(kMoments + kChecks);
+  launch_reduce(ra, bm, bc, st);
+  launch_sum_blocks(bc, kReduceBlocks, kChecks, outv + kMoments, st);
+  cuda_check(cudaGetLastError(), "validate launch");
+  double* h = static_cast<double*>(host_checks_.ensure(64 * sizeof(double)));
+  cuda_check(cudaMemcpyAsync(h, outv + kMoments, kChecks * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H checks");
+  cuda_check(cudaStreamSynchronize(st), "validate sync");
+  if (far_checks) require(h[0] == 0.0, ErrorCode::OutOfInterval, "source or target point outside the closed unit cell");
+  require(h[1] == 0.0, ErrorCode::NonUnitNormal, "stresslet normals must be unit vectors");
+  if (!pz_.requires_neutrality || !neutrality) return;  // apply.cpp:365-392
+  if (kind == Kind::Multipole)
+    require(std::hypot(h[7], h[8]) <= 1e-12 * h[9], ErrorCode::NotNeutral,
+            "this periodizer requires coefficients summing to zero");
+  else if (kind == Kind::Velocity)
+    require(std::hypot(h[4], h[5]) <= 1e-12 * h[6], ErrorCode::NotNeutral,
+            "this periodizer requires forces summing to zero");
+  else
+    require(std::abs(h[2]) <= 1e-12 * h[3], ErrorCode::NotNeutral, "this periodizer requires charges summing to zero");
+}
+
+void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff) {
+  cudaStream_t st = stream_for(o);
+  size_t off = 0;
+  for (const auto& fp : fams_) {
+    Family& f = *fp;
+    if (f.pressure && !o.with_pressure) continue;
+    const int k = weight_count(f.ws);
+    const size_t len = static_cast<size_t>(f.count) * k * 2;
+    f.raw_offset = off;
+    if (f.count > 0) {
+      const int chunks = s.ns == 0 ? 1 : s2pw_chunks(s.ns, f.count, k);
+      S2pwArgs a;
+      a.modes = f.table();
+      a.src = s.src;
+      a.q = s.q;
+      a.vec = f.ws == WeightSet::Coef ? s.coef : s.f;
+      a.nrm = s.nrm;
+      a.ns = s.ns;
+      a.chunks = chunks;
+      a.per_chunk = (s.ns + chunks - 1) / chunks;
+      a.partial = s2pw_partial_.as<double>(static_cast<size_t>(chunks) * len);
+      launch_s2pw(f.ws, a, st);
+      launch_chunk_sum(a.partial, chunks, len, coeff + off, st);
+    }
+    off += len;
+  }
+  // rank-one moments (apply.cpp:68-78, :108-117, :140-146, :179-191)
+  ReduceArgs ra;
+  ra.src = s.src;
+  ra.ns = s.ns;
+  ra.q = kind_of(pz_) == Kind::Scalar ? s.q : nullptr;
+  ra.vec = s.f;
+  ra.nrm = s.nrm;
+  double* bm = red_m_.as<double>(kReduceBlocks * kMoments);
+  double* bc = red_c_.as<double>(kReduceBlocks * kChecks);
+  launch_reduce(ra, bm, bc, st);
+  launch_sum_blocks(bm, kReduceBlocks, kMoments, coeff + off, st);
+  cuda_check(cudaGetLastError(), "source pass launch");
+}
+
+void Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out) {
+  cudaStream_t st = stream_for(o);
+  const Kind kind = kind_of(pz_);
+  // zero the outputs this kind produces, then every family accumulates
+  if (s.nt > 0) {
+    if (kind == Kind::Scalar) cuda_check(cudaMemsetAsync(out.scalar, 0, s.nt * sizeof(double), st), "memset");
+    if (kind == Kind::Multipole)
+      cuda_check(cudaMemsetAsync(out.complex_scalar, 0, 2 * s.nt * sizeof(double), st), "memset");
+    if (kind == Kind::Velocity) cuda_check(cudaMemsetAsync(out.velocity, 0, 2 * s.nt * sizeof(double), st), "memset");
+    if (o.with_pressure) cuda_check(cudaMemsetAsync(out.pressure, 0, s.nt * sizeof(double), st), "memset");
+    if (o.with_gradient) cuda_check(cudaMemsetAsync(out.gradient, 0, 2 * s.nt * sizeof(double), st), "memset");
+  }
+  size_t off = 0;
+  const size_t mom_off = coeff_size(o) - kMoments - 3;
+  for (const auto& fp : fams_) {
+    Family& f = *fp;
+    if (f.pressure && !o.with_pressure) continue;
+    const int k = weight_count(f.ws);
+    const size_t len = static_cast<size_t>(f.count) * k * 2;
+    double* A = A_.as<double>(static_cast<size_t>(std::max(f.count, 1)) * f.ko * 2);
+    double* B = B_.as<double>(static_cast<size_t>(std::max(f.count, 1)) * f.ko * 2);
+    double* m0 = m0_.as<double>(8);
+    PrepArgs pa;
+    pa.kind = f.kind;
+    pa.count = f.count;
+    pa.k = k;
+    pa.raw = coeff + off;
+    for (int i = 0; i < 6; ++i) {
+      const double* tp = static_cast<const double*>(f.t[i].get());
+      switch (i) {
+        case 0: pa.t0 = tp; break;
+        case 1: pa.t1 = tp; break;
+        case 2: pa.t2 = tp; break;
+        case 3: pa.t3 = tp; break;
+        case 4: pa.t4 = tp; break;
+        default: pa.t5 = tp; break;
+      }
+    }
+    pa.three_term = static_cast<const int*>(f.three_term.get());
+    pa.A = A;
+    pa.B = B;
+    launch_prep(pa, st);
+    if (f.has_lin || f.has_cst) {
+      const double* mv = f.has_lin ? f.mlin : nullptr;
+      if (f.has_lin)
+        m0_kernel<<<1, 32, 0, st>>>(coeff + mom_off, f.ia, f.ib, mv[0], mv[1], mv[2], mv[3], f.ko, m0);
+      else
+        m0_kernel<<<1, 32, 0, st>>>(coeff + mom_off, f.ia, f.ib, f.mcst[0], f.mcst[1], 0.0, 0.0, f.ko, m0);
+      count_launches(1);
+    }
+    Pw2tArgs ta;
+    ta.modes = f.table();
+    ta.A = A;
+    ta.B = (f.kind == FamilyKind::Block || f.kind == FamilyKind::Stresslet) ? B : nullptr;
+    ta.tgt = s.tgt;
+    ta.nt = s.nt;
+    ta.ko = f.ko;
+    ta.gradient = (f.kind == FamilyKind::Scalar && o.with_gradient) ? 1 : 0;
+    ta.m0_lin = f.has_lin ? m0 : nullptr;
+    ta.m0_const = f.has_cst ? m0 : nullptr;
+    ta.accumulate = 1;
+    if (f.kind == FamilyKind::Pressure) {
+      ta.out_re = out.pressure;
+    } else if (kind == Kind::Multipole) {
+      ta.out_cplx = out.complex_scalar;
+    } else if (kind == Kind::Velocity) {
+      ta.out_re = out.velocity;
+    } else {
+      ta.out_re = out.scalar;
+      ta.out_grad = out.gradient;
+    }
+    launch_pw2t(ta, st);
+    off += len;
+  }
+  cuda_check(cudaGetLastError(), "target pass launch");
+}
+
+void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
+                bool identity) {
+  if (s.nt == 0 || s.ns == 0) return;
+  cudaStream_t st = stream_for(o);
+  const Kind kind = kind_of(pz_);
+  NearKind nk;
+  NearArgs a;
+  a.tgt = s.tgt;
+  a.nt = s.nt;
+  a.src = s.src;
+  a.ns = s.ns;
+  a.q = s.q;
+  a.nrm = s.nrm;
+  a.vec = s.f;
+  a.beta = pz_.beta;
+  a.beta2 = pz_.beta * pz_.beta;
+  a.xcut2 = 64.0 * 64.0;  // K_0(x) < 3e-29 beyond: below fp64 resolution of any sum
+  if (kind == Kind::Multipole) {
+    nk = NearKind::Multipole;
+    a.vec = s.coef;
+    a.order = pz_.multipole_order;
+    a.screened = pz_.pde == periwave::Pde::ModHelmholtz ? 1 : 0;
+    a.out0 = out.complex_scalar;
+    a.nout0 = 2;
+  } else if (pz_.dlp) {
+    nk = NearKind::Stresslet;
+    a.out0 = out.velocity;
+    a.nout0 = 2;
+  } else if (kind == Kind::Velocity) {
+    const bool p = o.with_pressure;
+    nk = pz_.pde == periwave::Pde::Stokes ? (p ? NearKind::StokesP : NearKind::Stokes)
+                                          : (p ? NearKind::ModStokesP : NearKind::ModStokes);
+    a.ms_scale = pz_.pde == periwave::Pde::ModStokes ? 1.0 / (2.0 * periwave::kPi * a.beta2) : 0.0;
+    a.out0 = out.velocity;
+    a.nout0 = 2;
+    if (p) {
+      a.out1 = out.pressure;
+      a.nout1 = 1;
+    }
+  } else if (pz_.pde == periwave::Pde::ModHelmholtz) {
+    nk = o.with_gradient ? NearKind::ModHelmGrad : NearKind::ModHelm;
+    a.out0 = out.scalar;
+    a.nout0 = 1;
+    if (o.with_gradient) {
+      a.out1 = out.gradient;
+      a.nout1 = 2;
+    }
+  } else {
+    nk = NearKind::Laplace;
+    a.out0 = out.scalar;
+    a.nout0 = 1;
+  }
+  if (single) {
+    a.nxi = 1;
+    a.nrow = 1;
+    a.shx[0] = shx;
+    a.shy[0] = shy;
+    a.id_img = identity ? 0 : -1;
+  } else {
+    const periwave::UnitCell& c = pz_.cell;
+    if (c.periodicity == periwave::Periodicity::Doubly) {
+      a.nxi = 2 * c.m0 + 1;
+      a.nrow = 3;
+      for (int n = -1; n <= 1; ++n) {
+        a.shy[n + 1] = n * c.eta;
+        for (int m = -c.m0; m <= c.m0; ++m) a.shx[(n + 1) * a.nxi + (m + c.m0)] = m * c.d + n * c.xi;
+      }
+      a.id_img = 1 * a.nxi + c.m0;
+    } else {
+      a.nxi = 3;
+      a.nrow = 1;
+      a.shy[0] = 0.0;
+      for (int m = -1; m <= 1; ++m) a.shx[m + 1] = m * c.d;
+      a.id_img = 1;
+    }
+  }
+  int* flag = flag_.as<int>(1);
+  cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
+  a.flag = flag;
+  const size_t nout = near_outputs(nk);
+  double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
+  cuda_check(cudaEventRecord(ev_[2], st), "event");
+  launch_near(nk, a, st, ws, sms_);
+  cuda_check(cudaEventRecord(ev_[3], st), "event");
+  near_timed_ = true;
+  cuda_check(cudaGetLastError(), "near launch");
+  int* hflag = static_cast<int*>(host_checks_.ensure(64 * sizeof(double)));
+  cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+  cuda_check(cudaStreamSynchronize(st), "near sync");
+  require(*hflag == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
+}
+
+bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
+  bool accelerated = false;
+  cudaStream_t st = stream_for(o);
+  far_timed_ = near_timed_ = false;
+  if (far) {
+    validate(s, o, true);
+    double* coeff = coeff_ws_.as<double>(coeff_size(o));
+    cuda_check(cudaEventRecord(ev_[0], st), "event");
+    source_pass(s, o, coeff);
+    target_pass(s, o, coeff, out);
+    cuda_check(cudaEventRecord(ev_[1], st), "event");
+    far_timed_ = true;
+  }
+  if (near_images) {
+    if (!far) validate(s, o, false);
+    near(s, o, out, false, 0.0, 0.0, false);
+  }
+  return accelerated;
+}
+
+}  // namespace pwb

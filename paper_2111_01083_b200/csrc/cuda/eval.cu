@@ -1,0 +1,186 @@
+// Batch evaluation of the device pair math (pwb_eval_kernel), so parity tests
+// can pin the sm_100a Bessel/log/kernel functions point by point against the
+// reference's kernels.cpp:78-162.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "pw_engine.cuh"
+#include "pw_math.cuh"
+#include "pw_pair.cuh"
+
+namespace pwb {
+namespace {
+
+__device__ double bessel_kn_dev(int l, double x) {
+  if (!(x > 0.0)) return nan("");
+  if (x > 700.0) return 0.0;
+  const pwk::K01 k = pwk::k01_of_sq(x * x);
+  if (l == 0) return k.k0;
+  double km = k.k0, kc = k.k1_over_x * x;
+  for (int i = 1; i < l; ++i) {
+    const double kn = km + (2.0 * i / x) * kc;
+    km = kc;
+    kc = kn;
+  }
+  return kc;
+}
+
+__global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double inv2pi = 1.0 / (2.0 * pwk::kPi);
+  switch (which) {
+    case 0:
+      out[i] = bessel_kn_dev(l, in[i]);
+      break;
+    case 1: {
+      const double rx = in[2 * i], ry = in[2 * i + 1];
+      const double r2 = fma(rx, rx, ry * ry);
+      if (pde == 0)
+        out[i] = -0.5 * pwk::log_pos(r2) * inv2pi;
+      else
+        out[i] = (beta * beta * r2 < 4096.0 ? pwk::k0_of_sq(beta * beta * r2) : 0.0) * inv2pi;
+      break;
+    }
+    case 2: {
+      const double rx = in[2 * i], ry = in[2 * i + 1];
+      const double r2 = fma(rx, rx, ry * ry);
+      double g11, g12, g22;
+      if (pde == 2) {
+        const double c = -1.0 / (4.0 * pwk::kPi);
+        const double lg = 0.5 * pwk::log_pos(r2);
+        const double inv = pwk::rcp(r2);
+        g11 = c * (lg - rx * rx * inv);
+        g12 = c * (-rx * ry * inv);
+        g22 = c * (lg - ry * ry * inv);
+      } else {
+        const pwk::G12 g = pwk::mod_stokes_g12(beta * sqrt(r2));
+        const double inv = 1.0 / r2;
+        const double c = inv / (2.0 * pwk::kPi * beta * beta);
+        const double xh2 = rx * rx * inv, yh2 = ry * ry * inv, xy = rx * ry * inv;
+        g11 = c * (g.g2 * yh2 + g.g1 * xh2);
+        g22 = c * (g.g2 * xh2 + g.g1 * yh2);
+        g12 = -c * xy * (g.g2 - g.g1);
+      }
+      out[4 * i] = g11;
+      out[4 * i + 1] = g12;
+      out[4 * i + 2] = g12;
+      out[4 * i + 3] = g22;
+      break;
+    }
+    case 3: {
+      const double rx = in[2 * i], ry = in[2 * i + 1];
+      double pr = 1.0, pi = 0.0;
+      if (pde == 0) {
+        for (int k = 0; k < l; ++k) {
+          const double t = pr * rx - pi * ry;
+          pi = pr * ry + pi * rx;
+          pr = t;
+        }
+        const double d = pr * pr + pi * pi;
+        out[2 * i] = pr / d;
+        out[2 * i + 1] = -pi / d;
+      } else {
+        const double rr = sqrt(fma(rx, rx, ry * ry));
+        const double kl = bessel_kn_dev(l, beta * rr);
+        for (int k = 0; k < l; ++k) {
+          const double t = pr * (rx / rr) - pi * (ry / rr);
+          pi = pr * (ry / rr) + pi * (rx / rr);
+          pr = t;
+        }
+        out[2 * i] = kl * pr;
+        out[2 * i + 1] = kl * pi;
+      }
+      break;
+    }
+    case 4: {
+      const double rx = in[2 * i], ry = in[2 * i + 1];
+      const double r2 = fma(rx, rx, ry * ry);
+      out[2 * i] = rx * inv2pi / r2;
+      out[2 * i + 1] = ry * inv2pi / r2;
+      break;
+    }
+    case 5: {
+      const double rx = in[4 * i], ry = in[4 * i + 1], nx = in[4 * i + 2], ny = in[4 * i + 3];
+      const double r2 = fma(rx, rx, ry * ry);
+      const double c = -(rx * nx + ry * ny) / (pwk::kPi * r2 * r2);
+      out[4 * i] = c * rx * rx;
+      out[4 * i + 1] = c * rx * ry;
+      out[4 * i + 2] = c * rx * ry;
+      out[4 * i + 3] = c * ry * ry;
+      break;
+    }
+    default:
+      out[i] = nan("");
+  }
+}
+
+// 8 independent DFMA chains per thread; 2 flop per DFMA.
+__global__ void __launch_bounds__(256) dfma_chain_kernel(int iters, double seed, double* sink) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k * 1e-7;
+  const double m = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) sink[0] = s;  // never true; keeps the chains live
+}
+
+}  // namespace
+
+double fp64_peak_probe() {
+  int dev = 0, sms = 148;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  double* sink = nullptr;
+  cuda_check(cudaMalloc(&sink, sizeof(double)), "cudaMalloc");
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 1 << 14, blocks = sms * 8, threads = 256;
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0);
+    dfma_chain_kernel<<<blocks, threads>>>(iters, 1.0 + rep, sink);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaEventSynchronize(e1);
+    if (err != cudaSuccess) {
+      cudaFree(sink);
+      cuda_check(err, "dfma probe");
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    if (rep > 0 && ms > 0.f) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  count_launches(6);
+  return best;
+}
+
+int eval_in_width(int which) { return which == 0 ? 1 : which == 5 ? 4 : 2; }
+int eval_out_width(int which) { return which <= 1 ? 1 : (which == 3 || which == 4) ? 2 : 4; }
+
+void run_eval(int which, int pde, double beta, int l, size_t n, const double* in_host, double* out_host) {
+  const size_t nin = n * eval_in_width(which), nout = n * eval_out_width(which);
+  double *din = nullptr, *dout = nullptr;
+  cuda_check(cudaMalloc(&din, (nin + 1) * sizeof(double)), "cudaMalloc");
+  cuda_check(cudaMalloc(&dout, (nout + 1) * sizeof(double)), "cudaMalloc");
+  cuda_check(cudaMemcpy(din, in_host, nin * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+  eval_kernel<<<static_cast<unsigned>((n + 127) / 128), 128>>>(which, pde, beta, l, n, din, dout);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(out_host, dout, nout * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(din);
+  cudaFree(dout);
+  cuda_check(e, "eval kernel");
+}
+
+}  // namespace pwb

@@ -1,0 +1,516 @@
+// Near-image P2P tiles: every near lattice image fused into one launch.
+//
+// Replaces the reference's per-image double loop
+// (/root/reference/proj/src/apply.cpp:481-546, called once per image at :553-554)
+// and its pair kernels (kernels.cpp:98-162). One thread owns TPT targets in
+// registers; sources stream through shared memory in tiles (all lanes read
+// the same source -> broadcast, no bank conflicts); every (target, source)
+// pair is evaluated for all NXI x NROW images before moving on, so position
+// deltas, strengths and the log are shared across images:
+//   * Laplace / Stokeslet log terms: sum_img q log r2_img = q log(prod_img r2_img),
+//     one log per (target, source) instead of one per image;
+//   * zero-distance semantics of the reference (identity image skips exact
+//     zeros, any other image raises CoincidentSourceTarget) are kept exactly:
+//     a product that is 0/subnormal/inf falls to a per-image slow path.
+// Accumulation is fp64 in registers; with source splits the per-split partial
+// sums are combined in fixed order (deterministic for a given launch shape).
+#include <cuda_runtime.h>
+
+#include "pw_engine.cuh"
+#include "pw_math.cuh"
+#include "pw_pair.cuh"
+
+namespace pwb {
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kTile = 256;
+
+__device__ __forceinline__ bool normal_pos(double p) {
+  const int ex = (pwk::hi_of(p) >> 20) & 0x7ff;
+  return ex != 0 && ex != 0x7ff;
+}
+
+// ---------------------------------------------------------------- pair functors
+// Each functor: NW strength doubles per source, NACC accumulators per target,
+// NOUT output doubles per target, pair<NXI,NROW>(acc, dx, dy, w, args, flag),
+// finish(acc, args, out[NOUT]).
+
+struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
+  static constexpr int NW = 1, NACC = 1, NOUT = 1;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+    double ry2[NROW];
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+      ry2[n] = ry * ry;
+    }
+    double P = 1.0;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        P *= fma(rx, rx, ry2[n]);
+      }
+    if (normal_pos(P)) {
+      acc[0] = fma(w[0], pwk::log_pos(P), acc[0]);
+      return;
+    }
+    double L = 0.0;
+#pragma unroll 1
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll 1
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        const double ry = dy - a.shy[n];
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        L += pwk::log_r2_safe(rx, ry);
+      }
+    acc[0] = fma(w[0], L, acc[0]);
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    out[0] = acc[0] * (-1.0 / (4.0 * pwk::kPi));
+  }
+};
+
+struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
+  static constexpr int NW = 1, NACC = 1, NOUT = 1;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+      const double ry2 = ry * ry;
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        const double r2 = fma(rx, rx, ry2);
+        if (r2 == 0.0) {
+          if (rx == 0.0 && ry == 0.0) {
+            if (n * NXI + m != a.id_img) flag = 1;
+            continue;
+          }
+        }
+        const double X = a.beta2 * r2;
+        if (X < a.xcut2) acc[0] = fma(w[0], pwk::k0_of_sq(X), acc[0]);
+      }
+    }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
+  }
+};
+
+struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
+  static constexpr int NW = 1, NACC = 3, NOUT = 3;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+      const double ry2 = ry * ry;
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        const double r2 = fma(rx, rx, ry2);
+        if (r2 == 0.0) {
+          if (rx == 0.0 && ry == 0.0) {
+            if (n * NXI + m != a.id_img) flag = 1;
+            continue;
+          }
+        }
+        const double X = a.beta2 * r2;
+        if (X < a.xcut2) {
+          const pwk::K01 k = pwk::k01_of_sq(X);
+          acc[0] = fma(w[0], k.k0, acc[0]);
+          const double g = w[0] * k.k1_over_x;
+          acc[1] = fma(g, rx, acc[1]);
+          acc[2] = fma(g, ry, acc[2]);
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs& a, double* out) {
+    out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
+    const double gs = -a.beta2 / (2.0 * pwk::kPi);
+    out[1] = acc[1] * gs;
+    out[2] = acc[2] * gs;
+  }
+};
+
+// Stokeslet -(1/4pi)(log|r| I - r r^T/|r|^2) f  (kernels.cpp:115-119), plus the
+// optional pressurelet r.f/(2 pi r^2) (kernels.cpp:139-143).
+template <bool PRESSURE>
+struct Stokes {
+  static constexpr int NW = 2, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+    double P = 1.0;
+    double ax = 0.0, ay = 0.0, pr = 0.0;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+      const double ry2 = ry * ry;
+      const double fy_ry = w[1] * ry;
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        const double r2 = fma(rx, rx, ry2);
+        P *= r2;
+        const double t = fma(w[0], rx, fy_ry) * pwk::rcp(r2);
+        ax = fma(rx, t, ax);
+        ay = fma(ry, t, ay);
+        if (PRESSURE) pr += t;
+      }
+    }
+    if (normal_pos(P)) {
+      const double L = pwk::log_pos(P);
+      acc[0] = fma(L, w[0], acc[0]);
+      acc[1] = fma(L, w[1], acc[1]);
+      acc[2] += ax;
+      acc[3] += ay;
+      if (PRESSURE) acc[4] += pr;
+      return;
+    }
+    // slow path: exact per-image semantics (rare: coincident or extreme pairs)
+#pragma unroll 1
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll 1
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        const double ry = dy - a.shy[n];
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        const double r2 = fma(rx, rx, ry * ry);
+        const double L = pwk::log_r2_safe(rx, ry);
+        const double t = fma(w[0], rx, w[1] * ry) / r2;
+        acc[0] = fma(L, w[0], acc[0]);
+        acc[1] = fma(L, w[1], acc[1]);
+        acc[2] = fma(rx, t, acc[2]);
+        acc[3] = fma(ry, t, acc[3]);
+        if (PRESSURE) acc[4] += t;
+      }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    const double c = -1.0 / (4.0 * pwk::kPi);
+    out[0] = c * fma(0.5, acc[0], -acc[2]);
+    out[1] = c * fma(0.5, acc[1], -acc[3]);
+    if (PRESSURE) out[2] = acc[4] * (1.0 / (2.0 * pwk::kPi));
+  }
+};
+
+// Screened Stokeslet (kernels.cpp:120-130) through g1/g2 (kernels.cpp:36-68).
+template <bool PRESSURE>
+struct ModStokes {
+  static constexpr int NW = 2, NACC = PRESSURE ? 3 : 2, NOUT = PRESSURE ? 3 : 2;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+#pragma unroll 1
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+#pragma unroll 1
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        const double r2 = fma(rx, rx, ry * ry);
+        const double inv = 1.0 / r2;
+        const pwk::G12 g = pwk::mod_stokes_g12(a.beta * sqrt(r2));
+        const double c = inv * a.ms_scale;  // 1/(2 pi beta^2 r^2)
+        const double xh2 = rx * rx * inv, yh2 = ry * ry * inv, xy = rx * ry * inv;
+        const double g11 = c * (g.g2 * yh2 + g.g1 * xh2);
+        const double g22 = c * (g.g2 * xh2 + g.g1 * yh2);
+        const double g12 = -c * xy * (g.g2 - g.g1);
+        acc[0] += g11 * w[0] + g12 * w[1];
+        acc[1] += g12 * w[0] + g22 * w[1];
+        if (PRESSURE) acc[2] += fma(rx, w[0], ry * w[1]) * inv;
+      }
+    }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    out[0] = acc[0];
+    out[1] = acc[1];
+    if (PRESSURE) out[2] = acc[2] * (1.0 / (2.0 * pwk::kPi));
+  }
+};
+
+// Stresslet double layer -(1/pi) r r^T (r.n) f / |r|^4 (kernels.cpp:145-151).
+struct Stresslet {
+  static constexpr int NW = 4, NACC = 2, NOUT = 2;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        const double r2 = fma(rx, rx, ry * ry);
+        const double inv = pwk::rcp(r2);
+        const double c = fma(rx, w[2], ry * w[3]) * fma(rx, w[0], ry * w[1]) * inv * inv;
+        acc[0] = fma(c, rx, acc[0]);
+        acc[1] = fma(c, ry, acc[1]);
+      }
+    }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    out[0] = acc[0] * (-1.0 / pwk::kPi);
+    out[1] = acc[1] * (-1.0 / pwk::kPi);
+  }
+};
+
+// Multipole sources (kernels.cpp:153-162): Poisson 1/z^l, ModHelmholtz
+// K_l(beta r) (z/r)^l, complex strengths.
+struct Multipole {
+  static constexpr int NW = 2, NACC = 2, NOUT = 2;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
+                                              const NearArgs& a, int& flag) {
+#pragma unroll 1
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = dy - a.shy[n];
+#pragma unroll 1
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = dx - a.shx[n * NXI + m];
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        double vr, vi;
+        if (a.screened) {
+          const double r2 = fma(rx, rx, ry * ry);
+          const double rr = sqrt(r2);
+          const double x = a.beta * rr;
+          double kl;
+          if (x > 700.0) {
+            kl = 0.0;
+          } else {
+            const pwk::K01 k = pwk::k01_of_sq(x * x);
+            double km = k.k0, kc = k.k1_over_x * x;
+            for (int l = 1; l < a.order; ++l) {
+              const double kn = km + (2.0 * l / x) * kc;
+              km = kc;
+              kc = kn;
+            }
+            kl = kc;
+          }
+          // (z / r)^l
+          const double ux = rx / rr, uy = ry / rr;
+          double pr = 1.0, pi = 0.0;
+          for (int l = 0; l < a.order; ++l) {
+            const double t = pr * ux - pi * uy;
+            pi = pr * uy + pi * ux;
+            pr = t;
+          }
+          vr = kl * pr;
+          vi = kl * pi;
+        } else {
+          // 1 / z^l: z^l by repeated multiplication, then complex reciprocal
+          double pr = 1.0, pi = 0.0;
+          for (int l = 0; l < a.order; ++l) {
+            const double t = pr * rx - pi * ry;
+            pi = pr * ry + pi * rx;
+            pr = t;
+          }
+          const double d = pr * pr + pi * pi;
+          vr = pr / d;
+          vi = -pi / d;
+        }
+        acc[0] += vr * w[0] - vi * w[1];
+        acc[1] += vr * w[1] + vi * w[0];
+      }
+    }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    out[0] = acc[0];
+    out[1] = acc[1];
+  }
+};
+
+// ---------------------------------------------------------------- the tile kernel
+template <class KER, int NXI, int NROW, int TPT>
+__global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_constant__ NearArgs a) {
+  __shared__ double s_x[kTile];
+  __shared__ double s_y[kTile];
+  __shared__ double s_w[KER::NW][kTile];
+
+  const size_t block_t0 = static_cast<size_t>(blockIdx.x) * (kThreads * TPT);
+  double tx[TPT], ty[TPT], acc[TPT][KER::NACC];
+  bool live[TPT];
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const size_t l = block_t0 + threadIdx.x + k * kThreads;
+    live[k] = l < a.nt;
+    const double2 t = live[k] ? a.tgt[l] : make_double2(0.0, 0.0);
+    tx[k] = t.x;
+    ty[k] = t.y;
+#pragma unroll
+    for (int c = 0; c < KER::NACC; ++c) acc[k][c] = 0.0;
+  }
+  int flag = 0;
+
+  const size_t j_begin = static_cast<size_t>(blockIdx.y) * a.src_per_split;
+  size_t j_end = j_begin + a.src_per_split;
+  if (j_end > a.ns) j_end = a.ns;
+
+  for (size_t j0 = j_begin; j0 < j_end; j0 += kTile) {
+    const int tn = static_cast<int>((j_end - j0) < kTile ? (j_end - j0) : kTile);
+    __syncthreads();
+    for (int i = threadIdx.x; i < tn; i += kThreads) {
+      const double2 p = a.src[j0 + i];
+      s_x[i] = p.x;
+      s_y[i] = p.y;
+      if (KER::NW == 1) {
+        s_w[0][i] = a.q[j0 + i];
+      } else {
+        const double2 v = a.vec[j0 + i];
+        s_w[0][i] = v.x;
+        s_w[1 % KER::NW][i] = v.y;
+        if (KER::NW == 4) {
+          const double2 nn = a.nrm[j0 + i];
+          s_w[2 % KER::NW][i] = nn.x;
+          s_w[3 % KER::NW][i] = nn.y;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int i = 0; i < tn; ++i) {
+      const double sx = s_x[i], sy = s_y[i];
+      double w[KER::NW];
+#pragma unroll
+      for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        // (t - s) - shift, the reference's association (apply.cpp:534)
+        KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag);
+      }
+    }
+  }
+
+  if (flag) atomicOr(a.flag, 1);
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    if (!live[k]) continue;
+    const size_t l = block_t0 + threadIdx.x + k * kThreads;
+    double o[KER::NOUT];
+    KER::finish(acc[k], a, o);
+    if (a.splits == 1) {
+#pragma unroll
+      for (int c = 0; c < KER::NOUT; ++c) {
+        double* dst = c < a.nout0 ? a.out0 + l * a.nout0 + c : a.out1 + l * a.nout1 + (c - a.nout0);
+        *dst += o[c];
+      }
+    } else {
+      double* part = a.partial + (static_cast<size_t>(blockIdx.y) * a.nt + l) * KER::NOUT;
+#pragma unroll
+      for (int c = 0; c < KER::NOUT; ++c) part[c] = o[c];
+    }
+  }
+}
+
+// out += sum_split partial[split] in fixed split order.
+__global__ void near_reduce_kernel(const double* partial, int splits, size_t nt, int nout, double* out0, int nout0,
+                                   double* out1, int nout1) {
+  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= nt * nout) return;
+  const size_t l = idx / nout;
+  const int c = static_cast<int>(idx % nout);
+  double s = 0.0;
+  for (int sp = 0; sp < splits; ++sp) s += partial[static_cast<size_t>(sp) * nt * nout + idx];
+  double* dst = c < nout0 ? out0 + l * nout0 + c : out1 + l * nout1 + (c - nout0);
+  *dst += s;
+}
+
+template <class KER, int NXI, int NROW, int TPT>
+void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int sm_count) {
+  NearArgs a = a0;
+  const size_t per_block = static_cast<size_t>(kThreads) * TPT;
+  const unsigned bx = static_cast<unsigned>((a.nt + per_block - 1) / per_block);
+  // enough blocks to fill the chip ~4 deep; each split keeps >= 4 tiles of sources
+  int splits = 1;
+  const size_t want = static_cast<size_t>(sm_count) * 4;
+  if (bx < want && partial_ws != nullptr) {
+    splits = static_cast<int>((want + bx - 1) / bx);
+    const size_t max_by_src = (a.ns + 4 * kTile - 1) / (4 * kTile);
+    if (static_cast<size_t>(splits) > max_by_src) splits = static_cast<int>(max_by_src);
+    if (splits > kMaxSplits) splits = kMaxSplits;
+    if (splits < 1) splits = 1;
+  }
+  a.splits = splits;
+  a.src_per_split = (a.ns + splits - 1) / splits;
+  a.src_per_split = ((a.src_per_split + kTile - 1) / kTile) * kTile;
+  a.partial = partial_ws;
+  dim3 grid(bx, splits);
+  near_tile_kernel<KER, NXI, NROW, TPT><<<grid, kThreads, 0, st>>>(a);
+  count_launches(1);
+  if (splits > 1) {
+    const size_t n = a.nt * KER::NOUT;
+    near_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(partial_ws, splits, a.nt, KER::NOUT,
+                                                                               a.out0, a.nout0, a.out1, a.nout1);
+    count_launches(1);
+  }
+}
+
+template <class KER, int TPT>
+void dispatch_images(const NearArgs& a, cudaStream_t st, double* ws, int sms) {
+  if (a.nxi == 1 && a.nrow == 1) return launch_shape<KER, 1, 1, TPT>(a, st, ws, sms);
+  if (a.nxi == 3 && a.nrow == 1) return launch_shape<KER, 3, 1, TPT>(a, st, ws, sms);
+  if (a.nxi == 3 && a.nrow == 3) return launch_shape<KER, 3, 3, TPT>(a, st, ws, sms);
+  if (a.nxi == 5 && a.nrow == 3) return launch_shape<KER, 5, 3, TPT>(a, st, ws, sms);
+  if (a.nxi == 7 && a.nrow == 3) return launch_shape<KER, 7, 3, TPT>(a, st, ws, sms);
+  throw_internal("near field: unsupported image layout");
+}
+
+}  // namespace
+
+size_t near_outputs(NearKind kind) {
+  switch (kind) {
+    case NearKind::Laplace:
+    case NearKind::ModHelm: return 1;
+    case NearKind::ModHelmGrad: return 3;
+    case NearKind::Stokes:
+    case NearKind::ModStokes:
+    case NearKind::Stresslet:
+    case NearKind::Multipole: return 2;
+    case NearKind::StokesP:
+    case NearKind::ModStokesP: return 3;
+  }
+  return 1;
+}
+
+void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count) {
+  if (a.nt == 0 || a.ns == 0) return;
+  switch (kind) {
+    case NearKind::Laplace: return dispatch_images<Laplace, 2>(a, st, partial_ws, sm_count);
+    case NearKind::ModHelm: return dispatch_images<ModHelm, 1>(a, st, partial_ws, sm_count);
+    case NearKind::ModHelmGrad: return dispatch_images<ModHelmGrad, 1>(a, st, partial_ws, sm_count);
+    case NearKind::Stokes: return dispatch_images<Stokes<false>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::StokesP: return dispatch_images<Stokes<true>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::ModStokes: return dispatch_images<ModStokes<false>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::ModStokesP: return dispatch_images<ModStokes<true>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::Stresslet: return dispatch_images<Stresslet, 1>(a, st, partial_ws, sm_count);
+    case NearKind::Multipole: return dispatch_images<Multipole, 1>(a, st, partial_ws, sm_count);
+  }
+}
+
+}  // namespace pwb

@@ -1,0 +1,157 @@
+// Internal device-engine interface shared by the kernel translation units and
+// the host orchestration (engine.cu). Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace pwb {
+
+constexpr int kMaxImg = 21;   // doubly periodic m0 <= 3: 7 x 3 images
+constexpr int kMaxSplits = 64;
+
+struct CudaFailure : std::runtime_error {
+  explicit CudaFailure(const std::string& s) : std::runtime_error(s) {}
+};
+struct InternalFailure : std::runtime_error {
+  explicit InternalFailure(const std::string& s) : std::runtime_error(s) {}
+};
+[[noreturn]] void throw_internal(const char* what);
+void cuda_check(cudaError_t e, const char* what);
+// Number of kernels this process has launched through the engine (pwb_launch_count).
+void count_launches(long n);
+long launch_count();
+
+// ---------------------------------------------------------------- near field
+enum class NearKind { Laplace, ModHelm, ModHelmGrad, Stokes, StokesP, ModStokes, ModStokesP, Stresslet, Multipole };
+
+struct NearArgs {
+  const double2* tgt = nullptr;
+  size_t nt = 0;
+  const double2* src = nullptr;
+  size_t ns = 0;
+  const double* q = nullptr;       // charges
+  const double2* vec = nullptr;    // forces or complex coefficients
+  const double2* nrm = nullptr;    // normals (stresslet)
+  double shx[kMaxImg] = {};        // row-major [n][m]: m*d + n*xi (reference association)
+  double shy[3] = {};              // n*eta
+  int nxi = 1, nrow = 1, id_img = -1;
+  double beta = 0.0, beta2 = 0.0, xcut2 = 0.0, ms_scale = 0.0;
+  int order = 0, screened = 0;
+  double* out0 = nullptr;  // first nout0 outputs, interleaved per target
+  int nout0 = 1;
+  double* out1 = nullptr;  // remaining outputs (gradient / pressure)
+  int nout1 = 0;
+  double* partial = nullptr;
+  int splits = 1;
+  size_t src_per_split = 0;
+  int* flag = nullptr;     // set to 1 on a non-identity exact coincidence
+};
+
+size_t near_outputs(NearKind kind);
+void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count);
+
+// ---------------------------------------------------------------- far field (direct S2PW / PW2T)
+// Weight sets: what each source contributes per mode (K real weights).
+enum class WeightSet { Charge = 1, Coef = 2, Force = 3, ForceW = 4, DoubleLayer = 5 };
+
+inline int weight_count(WeightSet w) {
+  switch (w) {
+    case WeightSet::Charge: return 1;
+    case WeightSet::Coef:
+    case WeightSet::Force: return 2;
+    case WeightSet::ForceW: return 4;
+    case WeightSet::DoubleLayer: return 8;
+  }
+  return 1;
+}
+
+struct ModeTable {  // device SoA, one entry per mode of a family
+  const double* phase = nullptr;
+  const double* decay_t = nullptr;
+  const double* decay_s = nullptr;
+  const double* shift_t = nullptr;
+  const double* shift_s = nullptr;
+  const int* axis = nullptr;  // 0 vertical (w = y, p = x), 1 horizontal (w = x, p = y)
+  int count = 0;
+};
+
+struct S2pwArgs {
+  ModeTable modes;
+  const double2* src = nullptr;
+  const double* q = nullptr;
+  const double2* vec = nullptr;
+  const double2* nrm = nullptr;
+  size_t ns = 0;
+  size_t per_chunk = 0;
+  int chunks = 1;
+  double* partial = nullptr;  // [chunk][mode][K][2]
+};
+void launch_s2pw(WeightSet ws, const S2pwArgs& a, cudaStream_t st);
+// sums partial over chunks (fixed order) into raw[mode][K][2]
+void launch_chunk_sum(const double* partial, int chunks, size_t per_chunk_len, double* raw, cudaStream_t st);
+
+// target side: acc += T_l(r) (A_r + w_l B_r), KO complex outputs per target
+struct Pw2tArgs {
+  ModeTable modes;
+  const double* A = nullptr;  // [mode][KO][2]
+  const double* B = nullptr;  // [mode][KO][2] or nullptr
+  const double2* tgt = nullptr;
+  size_t nt = 0;
+  int ko = 1;
+  int gradient = 0;             // scalar family only: also d/dx, d/dy
+  const double* m0_lin = nullptr;    // [KO][2] device, acc += y * m0_lin (nullable)
+  const double* m0_const = nullptr;  // [KO][2] device, acc += m0_const (nullable)
+  // outputs: Re of each complex component, or complex pairs
+  double* out_re = nullptr;     // real output, KO per target (overwrite or add)
+  double* out_cplx = nullptr;   // complex output, KO complex per target
+  double* out_grad = nullptr;   // gradient (2 per target)
+  int accumulate = 0;           // add into outputs instead of overwriting
+};
+void launch_pw2t(const Pw2tArgs& a, cudaStream_t st);
+
+// per-mode finalisation of the raw source sums into target coefficients A/B
+enum class FamilyKind { Scalar = 0, Block = 1, Pressure = 2, Stresslet = 3 };
+struct PrepArgs {
+  FamilyKind kind = FamilyKind::Scalar;
+  int count = 0;
+  int k = 1;            // weights per source
+  const double* raw = nullptr;   // [mode][K][2]
+  const double* t0 = nullptr;    // family tables (see engine.cu)
+  const double* t1 = nullptr;
+  const double* t2 = nullptr;
+  const double* t3 = nullptr;
+  const double* t4 = nullptr;
+  const double* t5 = nullptr;
+  const int* three_term = nullptr;  // block: per mode flag
+  double* A = nullptr;
+  double* B = nullptr;
+};
+void launch_prep(const PrepArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- reductions / validation
+// moments over sources: [sum y q, sum y fx, sum y fy, sum n2 fx + n1 fy, sum n1 fx + n2 fy]
+constexpr int kMoments = 5;
+// validation: [bad points, bad normals, sum q, sum |q|, sum fx, sum fy, sum |f|, sum re c, sum im c, sum |c|]
+constexpr int kChecks = 10;
+struct ReduceArgs {
+  const double2* src = nullptr;
+  const double* q = nullptr;
+  const double2* vec = nullptr;  // forces
+  const double2* coef = nullptr;
+  const double2* nrm = nullptr;
+  size_t ns = 0;
+  const double2* tgt = nullptr;
+  size_t nt = 0;
+  double d = 1.0, xi = 0.0, eta = 1.0;
+};
+constexpr int kReduceBlocks = 296;
+// writes per-block partials: moments [blocks][kMoments], checks [blocks][kChecks]
+void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_checks, cudaStream_t st);
+void launch_sum_blocks(const double* block_vals, int blocks, int n, double* out, cudaStream_t st);
+
+}  // namespace pwb

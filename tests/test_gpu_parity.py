@@ -1,0 +1,315 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the compiled reference
+(oracle/_ref) and the C restatement (oracle/port) on identical seeded inputs.
+
+Bar (BASELINE.json north_star): relative l2 <= 10*eps per output channel, after
+removing the per-channel mean for Poisson potentials and Stokes velocities
+(gauge). Kernel point values are held to ~1e-14 relative.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _cell(pw, c):
+    return pw.make_unit_cell(c[0], c[1], c[2], pw.Periodicity(int(c[3])))
+
+
+# ------------------------------------------------------------------ device pair math
+def test_bessel_device_vs_reference(pw, gpu, ref):
+    xs = np.concatenate([np.geomspace(1e-6, 1.999, 300), [2.0, 2.0000001], np.geomspace(2.0001, 690.0, 400)])
+    for l in (0, 1, 2, 3):
+        got = pw.eval_kernel(0, 0, 0.0, l, xs)
+        want = np.array([ref.bessel_kn(l, x) for x in xs])
+        ok = want > 1e-300
+        rel = np.abs(got[ok] - want[ok]) / want[ok]
+        assert rel.max() < 2e-14, (l, xs[ok][np.argmax(rel)], rel.max())
+    # reference known answers (proj/tests/test_kernels.cpp:28-48)
+    k = pw.eval_kernel(0, 0, 0.0, 0, np.array([1.0, 800.0]))
+    assert abs(k[0] - 0.42102443824070833) <= 1e-14 * 0.42102443824070833
+    assert k[1] == 0.0
+    assert abs(pw.eval_kernel(0, 0, 0.0, 1, np.array([1.0]))[0] - 0.60190723019723457) <= 1e-14
+    assert abs(pw.eval_kernel(0, 0, 0.0, 2, np.array([1.3]))[0] - 0.85139763957996879) <= 1e-14
+    assert abs(pw.eval_kernel(0, 0, 0.0, 3, np.array([0.55]))[0] - 46.328915013455511) <= 1e-14 * 46.33
+
+
+def test_pair_kernels_device_vs_reference(pw, gpu, ref):
+    rng = np.random.default_rng(5)
+    r = rng.uniform(-2.5, 2.5, size=(500, 2))
+    r = r[np.hypot(r[:, 0], r[:, 1]) > 1e-3]
+    small = rng.uniform(-0.3, 0.3, size=(100, 2)) * 0.2  # ModStokes series branch
+    # Poisson / ModHelmholtz scalar (kernels.cpp:98-110)
+    for pde, beta in ((0, 0.0), (1, 2.5), (1, 10.0)):
+        got = pw.eval_kernel(1, pde, beta, 0, r)
+        want = np.array([ref.greens_scalar(pde, beta, v) for v in r])
+        assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)) < 5e-14 or \
+            np.max(np.abs(got - want)) < 1e-15
+    # Stokeslet and screened Stokeslet blocks (kernels.cpp:112-130)
+    for pde, beta, pts in ((2, 0.0, r), (3, 1.3, r), (3, 1.3, small)):
+        got = pw.eval_kernel(2, pde, beta, 0, pts)
+        want = np.array([ref.greens_block(pde, beta, v) for v in pts])
+        assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want)), pde
+    # multipole, pressurelet, stresslet
+    for pde, beta, l in ((0, 0.0, 2), (1, 1.1, 3), (1, 1.1, 1)):
+        got = pw.eval_kernel(3, pde, beta, l, r)
+        want = np.array([ref.multipole_kernel(pde, beta, l, v) for v in r])
+        assert np.max(np.abs(got[:, 0] + 1j * got[:, 1] - want) / np.abs(want)) < 1e-13
+    got = pw.eval_kernel(4, 0, 0.0, 0, r)
+    want = np.array([ref.pressurelet(v) for v in r])
+    assert np.max(np.abs(got - want)) <= 1e-14 * np.max(np.abs(want))
+    nrm = rng.normal(size=(len(r), 2))
+    nrm /= np.hypot(nrm[:, 0], nrm[:, 1])[:, None]
+    got = pw.eval_kernel(5, 0, 0.0, 0, np.concatenate([r, nrm], axis=1))
+    want = np.array([ref.stresslet_dlp(v, n) for v, n in zip(r, nrm)])
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
+# ------------------------------------------------------------------ the five configs at small N
+SMALL = {"c1": 1000, "c2": 1500, "c3": 1500, "c4": 2000, "c5": 3000}
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_config_small_total_field_vs_reference(pw, gpu, ref, name):
+    from paper_2111_01083_b200 import configs
+
+    inp = configs.generate(name, n_src=SMALL[name])
+    c = inp.config
+    cell = _cell(pw, c.cell)
+    pz = pw.make_periodizer(c.pde, c.beta, cell, c.eps)
+    R = ref.make_periodizer(int(c.pde), c.beta, tuple(float(v) for v in c.cell[:3]) + (int(c.cell[3]),), c.eps)
+    tgt = np.ascontiguousarray(inp.targets[inp.sample[:400]])
+    kw = dict(charges=inp.charges) if c.strength == "charge" else dict(forces=inp.forces)
+    sysd = pw.ParticleSystem(sources=inp.sources, targets=tgt, **kw)
+    opt = pw.ApplyOptions(path=pw.ApplyPath.Direct, with_gradient=c.gradient)
+    got = pw.total_field(pz, sysd, opt)
+    want = R.apply(0, inp.sources, tgt, path=1, threads=8, **kw)
+    gauge = c.pde in (pw.Pde.Poisson, pw.Pde.Stokes)
+    if c.strength == "charge":
+        err = rel_l2(got.scalar, want["scalar"], gauge)
+    else:
+        err = rel_l2(got.velocity, want["velocity"], gauge)
+    assert err <= 10 * c.eps, (name, err)
+    if c.gradient:  # l = 1 multipole periodizer oracle
+        M = ref.make_multipole_periodizer(int(c.pde), c.beta, 1, tuple(float(v) for v in c.cell[:3]) +
+                                          (int(c.cell[3]),), c.eps)
+        coef = np.stack([inp.charges, np.zeros_like(inp.charges)], -1)
+        cs = M.apply(0, inp.sources, tgt, coefficients=coef, path=1, threads=8)["complex"]
+        g_want = -(c.beta / (2 * np.pi)) * cs
+        gerr = rel_l2(got.gradient, g_want, False)
+        assert gerr <= 10 * c.eps, (name, "gradient", gerr)
+
+
+# ------------------------------------------------------------------ near / far separately, all kernels
+KERNEL_CASES = [
+    ("poisson-square", 0, 0.0, (1.0, 0.0, 1.0, 2), 1e-10, "charge", True),
+    ("poisson-skew", 0, 0.0, (1.0, 0.35, 0.8, 2), 1e-10, "charge", True),
+    ("poisson-strip", 0, 0.0, (1.0, 0.2, 1.5, 1), 1e-10, "charge", True),
+    ("mhelm-wide", 1, 1.0, (1.0, 0.0, 1.0 / 12.0, 2), 1e-12, "charge", False),
+    ("mhelm-skew3", 1, 2.0, (1.0, 0.6, 0.75, 2), 1e-10, "charge", False),
+    ("stokes-skew", 2, 0.0, (1.0, 0.3, 0.8, 2), 1e-8, "force", True),
+    ("stokes-strip", 2, 0.0, (1.0, 0.0, 2.0, 1), 1e-8, "force", True),
+    ("mstokes", 3, 1.5, (1.0, 0.2, 0.9, 2), 1e-10, "force", False),
+]
+
+
+def _system(rng, cell, ns, nt, strength, neutral):
+    d, xi, eta = cell[:3]
+
+    def pts(n):
+        a = rng.uniform(-0.5, 0.5, n)
+        b = rng.uniform(-0.5, 0.5, n)
+        return np.ascontiguousarray(np.stack([a * d + b * xi, b * eta], 1))
+
+    src, tgt = pts(ns), pts(nt)
+    if strength == "charge":
+        q = rng.uniform(-1, 1, ns)
+        if neutral:
+            q -= q.mean()
+        return src, tgt, dict(charges=np.ascontiguousarray(q))
+    f = rng.uniform(-1, 1, (ns, 2))
+    if neutral:
+        f -= f.mean(axis=0)
+    return src, tgt, dict(forces=np.ascontiguousarray(f))
+
+
+@pytest.mark.parametrize("case", KERNEL_CASES, ids=[c[0] for c in KERNEL_CASES])
+@pytest.mark.parametrize("pressure", [False, True])
+def test_near_and_far_vs_reference(pw, gpu, ref, case, pressure):
+    name, pde, beta, cell, eps, strength, neutral = case
+    if pressure and strength != "force":
+        pytest.skip("pressure is a Stokes-family output")
+    rng = np.random.default_rng(abs(hash(name)) % 2**32)
+    src, tgt, kw = _system(rng, cell, 700, 300, strength, neutral)
+    pz = pw.make_periodizer(pw.Pde(pde), beta, _cell(pw, cell), eps)
+    R = ref.make_periodizer(pde, beta, cell, eps)
+    opt = pw.ApplyOptions(path=pw.ApplyPath.Direct, with_pressure=pressure)
+    gauge = pde in (0, 2)
+    for mode, fn in ((1, pw.apply_far), (2, pw.near_field)):
+        got = fn(pz, pw.ParticleSystem(sources=src, targets=tgt, **kw), opt)
+        want = R.apply(mode, src, tgt, path=1, threads=8, with_pressure=pressure, **kw)
+        if strength == "charge":
+            err = rel_l2(got.scalar, want["scalar"], gauge and mode == 1)
+        else:
+            err = rel_l2(got.velocity, want["velocity"], gauge and mode == 1)
+        tol = 10 * eps if mode == 1 else 1e-13
+        assert err <= tol, (name, mode, err)
+        if pressure:
+            perr = rel_l2(got.pressure, want["pressure"], mode == 1)
+            assert perr <= (10 * eps if mode == 1 else 1e-13), (name, mode, "pressure", perr)
+
+
+def test_multipole_and_dlp_vs_reference(pw, gpu, ref):
+    rng = np.random.default_rng(11)
+    cell = (1.0, 0.0, 1.0, 2)
+    src, tgt, _ = _system(rng, cell, 500, 200, "charge", False)
+    for pde, beta, l in ((1, 1.5, 1), (1, 1.5, 3), (0, 0.0, 2)):
+        coef = rng.uniform(-1, 1, (500, 2))
+        pz = pw.make_multipole_periodizer(pw.Pde(pde), beta, l, _cell(pw, cell), 1e-10)
+        R = ref.make_multipole_periodizer(pde, beta, l, cell, 1e-10)
+        got = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=tgt, coefficients=np.ascontiguousarray(coef)),
+                             pw.ApplyOptions(path=pw.ApplyPath.Direct))
+        want = R.apply(0, src, tgt, coefficients=coef, path=1, threads=8)["complex"]
+        assert rel_l2(got.complex_scalar, want) <= 1e-9, (pde, l)
+    # Stokes double layer (stresslet), neutral forces, unit normals
+    f = rng.uniform(-1, 1, (500, 2))
+    f -= f.mean(axis=0)
+    n = rng.normal(size=(500, 2))
+    n /= np.hypot(n[:, 0], n[:, 1])[:, None]
+    pz = pw.make_stokes_dlp_periodizer(_cell(pw, cell), 1e-8)
+    R = ref.make_stokes_dlp_periodizer(cell, 1e-8)
+    sysd = pw.ParticleSystem(sources=src, targets=tgt, forces=np.ascontiguousarray(f), normals=np.ascontiguousarray(n))
+    got = pw.total_field(pz, sysd, pw.ApplyOptions(path=pw.ApplyPath.Direct))
+    want = R.apply(0, src, tgt, forces=f, normals=n, path=1, threads=8)["velocity"]
+    assert rel_l2(got.velocity, want, True) <= 1e-7
+
+
+def test_reference_tables_injected(pw, gpu, ref):
+    """Kernels fed the reference's own tables (pwb_periodizer_add_part) give the reference field."""
+    rng = np.random.default_rng(3)
+    cell = (1.0, 0.3, 0.8, 2)
+    src, tgt, kw = _system(rng, cell, 600, 250, "charge", False)
+    R = ref.make_periodizer(1, 10.0, cell, 1e-10)
+    pz = pw.Periodizer.from_tables(pw.Pde.ModHelmholtz, 10.0, _cell(pw, cell), 1e-10, R.all_parts())
+    got = pw.apply_far(pz, pw.ParticleSystem(sources=src, targets=tgt, **kw), pw.ApplyOptions(path=pw.ApplyPath.Direct))
+    want = R.apply(1, src, tgt, path=1, threads=8, **kw)["scalar"]
+    assert rel_l2(got.scalar, want) <= 1e-12
+
+
+# ------------------------------------------------------------------ edge semantics (proj/tests/test_apply.cpp)
+def test_empty_systems(pw, gpu):
+    cell = pw.make_unit_cell(1.0, 0.0, 1.0)
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, cell, 1e-10)
+    tgt = np.array([[0.1, 0.2], [-0.3, 0.4]])
+    r = pw.total_field(pz, pw.ParticleSystem(sources=np.zeros((0, 2)), charges=np.zeros(0), targets=tgt))
+    assert r.scalar.shape == (2,) and np.all(r.scalar == 0.0)
+    r = pw.apply_far(pz, pw.ParticleSystem(sources=tgt.copy(), charges=np.ones(2), targets=np.zeros((0, 2))))
+    assert r.scalar.shape == (0,)
+    zero = pw.total_field(pz, pw.ParticleSystem(sources=tgt.copy(), charges=np.zeros(2), targets=tgt))
+    assert np.all(zero.scalar == 0.0)
+
+
+def test_self_pairs_and_coincidence(pw, gpu, ref):
+    rng = np.random.default_rng(204)
+    cell = pw.make_unit_cell(1.0, 0.0, 1.0)
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, cell, 1e-10)
+    src = rng.uniform(-0.45, 0.45, (6, 2))
+    q = rng.uniform(-1, 1, 6)
+    f = pw.total_field(pz, pw.ParticleSystem(sources=src, charges=q, targets=src.copy()))
+    assert np.all(np.isfinite(f.scalar))
+    R = ref.make_periodizer(1, 1.0, (1.0, 0.0, 1.0, 2), 1e-10)
+    want = R.apply(0, src, src, charges=q, path=1)["scalar"]
+    assert rel_l2(f.scalar, want) <= 1e-12
+    # a target on a near image of a source: CoincidentSourceTarget
+    with pytest.raises(pw.PeriwaveError) as e:
+        pw.total_field(pz, pw.ParticleSystem(sources=np.array([[0.25, -0.5]]), charges=np.array([1.0]),
+                                             targets=np.array([[0.25, 0.5]])))
+    assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
+    strip = pw.make_unit_cell(1.0, 0.0, 1.5, pw.Periodicity.Singly)
+    pzs = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, strip, 1e-10)
+    with pytest.raises(pw.PeriwaveError) as e:
+        pw.total_field(pzs, pw.ParticleSystem(sources=np.array([[-0.5, 0.2]]), charges=np.array([1.0]),
+                                              targets=np.array([[0.5, 0.2]])))
+    assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
+
+
+def test_validation_errors(pw, gpu):
+    cell = pw.make_unit_cell(1.0, 0.0, 1.0)
+    pzp = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-10)
+    pzm = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, cell, 1e-10)
+    pzs = pw.make_periodizer(pw.Pde.Stokes, 0.0, cell, 1e-8)
+    src = np.array([[0.1, 0.1], [-0.2, 0.3]])
+    tgt = np.array([[0.0, 0.0]])
+    cases = [
+        (pzp, pw.ParticleSystem(sources=src, charges=np.array([1.0, 0.5]), targets=tgt), pw.ErrorCode.NotNeutral),
+        (pzm, pw.ParticleSystem(sources=src, charges=np.array([1.0, 0.5]), targets=np.array([[0.7, 0.0]])),
+         pw.ErrorCode.OutOfInterval),
+        (pzm, pw.ParticleSystem(sources=src, targets=tgt), pw.ErrorCode.LengthMismatch),
+        (pzs, pw.ParticleSystem(sources=src, charges=np.array([1.0, -1.0]), targets=tgt), pw.ErrorCode.LengthMismatch),
+    ]
+    for pz, s, code in cases:
+        with pytest.raises(pw.PeriwaveError) as e:
+            pw.total_field(pz, s)
+        assert e.value.code == code
+    with pytest.raises(pw.PeriwaveError) as e:
+        pw.apply_far(pzm, pw.ParticleSystem(sources=src, charges=np.array([1.0, 0.5]), targets=tgt),
+                     pw.ApplyOptions(with_pressure=True))
+    assert e.value.code == pw.ErrorCode.Unsupported
+
+
+def test_accumulate_single_image_vs_reference(pw, gpu, ref):
+    rng = np.random.default_rng(9)
+    cellt = (1.0, 0.4, 0.7, 2)
+    src, tgt, kw = _system(rng, cellt, 400, 150, "force", True)
+    pz = pw.make_periodizer(pw.Pde.ModStokes, 1.3, _cell(pw, cellt), 1e-10)
+    R = ref.make_periodizer(3, 1.3, cellt, 1e-10)
+    for shift, ident in (((0.0, 0.0), True), ((1.4, 0.7), False), ((-2.0, 0.0), False)):
+        out = pw.FieldResult(velocity=np.zeros((150, 2)), pressure=np.zeros(150))
+        pw.accumulate(pz, pw.ParticleSystem(sources=src, targets=tgt, **kw), shift, ident,
+                      pw.ApplyOptions(with_pressure=True), out)
+        want = R.accumulate(src, tgt, shift, ident, with_pressure=True, **kw)
+        assert rel_l2(out.velocity, want["velocity"]) <= 1e-13
+        assert rel_l2(out.pressure, want["pressure"]) <= 1e-13
+
+
+def test_deterministic_and_device_pointers(pw, gpu):
+    import torch
+    from paper_2111_01083_b200 import configs
+
+    inp = configs.generate("c4", n_src=20000)
+    c = inp.config
+    pz = pw.make_periodizer(c.pde, c.beta, _cell(pw, c.cell), c.eps)
+    host = pw.ParticleSystem(sources=inp.sources, charges=inp.charges, targets=inp.targets)
+    a = pw.total_field(pz, host, pw.ApplyOptions(path=pw.ApplyPath.Direct)).scalar
+    b = pw.total_field(pz, host, pw.ApplyOptions(path=pw.ApplyPath.Direct)).scalar
+    assert np.array_equal(a, b)
+    dev = pw.ParticleSystem(sources=torch.from_numpy(inp.sources).cuda(), charges=torch.from_numpy(inp.charges).cuda(),
+                            targets=torch.from_numpy(inp.targets).cuda())
+    d = pw.total_field(pz, dev, pw.ApplyOptions(path=pw.ApplyPath.Direct)).scalar.cpu().numpy()
+    assert np.array_equal(a, d)
+
+
+def test_sharded_far_equals_unsharded(pw, gpu):
+    """Source-sharded S2PW + summed coefficient buffers == one-shot apply_far (the NCCL allreduce
+    operand is linear in the sources). Shards run one after another on one GPU."""
+    import torch
+    from paper_2111_01083_b200 import configs
+
+    inp = configs.generate("c3", n_src=6000)
+    c = inp.config
+    pz = pw.make_periodizer(c.pde, c.beta, _cell(pw, c.cell), c.eps)
+    src = torch.from_numpy(inp.sources).cuda()
+    f = torch.from_numpy(inp.forces).cuda()
+    tgt = torch.from_numpy(inp.targets[:1000].copy()).cuda()
+    n = pw.far_coeff_size(pz)
+    total = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for lo, hi in ((0, 2500), (2500, 6000)):
+        part = torch.zeros(n, dtype=torch.float64, device="cuda")
+        pw.far_source_pass(pz, pw.ParticleSystem(sources=src[lo:hi], forces=f[lo:hi]), part)
+        total += part
+    got = pw.far_target_pass(pz, pw.ParticleSystem(sources=src, forces=f, targets=tgt), total).velocity.cpu().numpy()
+    want = pw.apply_far(pz, pw.ParticleSystem(sources=inp.sources, forces=inp.forces,
+                                              targets=np.ascontiguousarray(inp.targets[:1000])),
+                        pw.ApplyOptions(path=pw.ApplyPath.Direct)).velocity
+    assert rel_l2(got, want, True) <= 1e-12
