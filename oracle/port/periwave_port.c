@@ -39,10 +39,11 @@ static void series01(double x, double* k0, double* k1) {
 }
 
 static double trap_k(int n, double x) {
-  const double hstep = 0.125;
-  double acc = 0.5 * exp(0.0);
-  for (int k = 1; k < 4000; ++k) {
-    const double t = k * hstep, a = x * (cosh(t) - 1.0);
+  /* step ~ 1/sqrt(x) (Gaussian width), cosh t - 1 = 2 sinh^2(t/2) without cancellation */
+  const double hstep = fmin(0.125, 0.5 / sqrt(x));
+  double acc = 0.5;
+  for (int k = 1; k < 100000; ++k) {
+    const double t = k * hstep, sh = sinh(0.5 * t), a = 2.0 * x * sh * sh;
     acc += n == 0 ? exp(-a) : exp(-a) * cosh(n * t);
     if (a - n * t > 45.0) break;
   }

@@ -13,6 +13,7 @@
 //              e^x K_n(x) = int_0^inf exp(-x (cosh t - 1)) cosh(n t) dt, which
 //              converges geometrically in the step (the integrand is entire and
 //              bounded on the strip |Im t| < pi/2).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -58,12 +59,16 @@ void series_k01(double x, double* k0, double* k1) {
   *k1 = 1.0 / x + lhalf * I1 - 0.25 * x * s1;
 }
 
+// Step shrinks like 1/sqrt(x): the integrand is a Gaussian of width ~1/sqrt(x) and
+// the strip of analyticity that controls the error narrows the same way.
+// x (cosh t - 1) = 2 x sinh^2(t/2) avoids the cancellation at small t.
 double trapezoid_scaled(int n, double x) {
-  const double h = 0.125;
+  const double h = std::min(0.125, 0.5 / std::sqrt(x));
   double acc = 0.5;  // t = 0 contributes 1/2 * exp(0) * cosh(0)
-  for (int k = 1; k < 4000; ++k) {
+  for (int k = 1; k < 100000; ++k) {
     const double t = k * h;
-    const double a = x * (std::cosh(t) - 1.0);
+    const double sh = std::sinh(0.5 * t);
+    const double a = 2.0 * x * sh * sh;
     const double e = a - n * t;
     acc += (n == 0) ? std::exp(-a) : std::exp(-a) * std::cosh(n * t);
     if (e > 45.0) break;

@@ -147,7 +147,12 @@ void stage_in(pwb::Plan& p, const pwb_system* s, cudaStream_t st, pwb::DevSys* d
   ds->f = put(p.stage[2], s->forces, 2 * s->n_src, st);
   ds->nrm = put(p.stage[3], s->normals, 2 * s->n_src, st);
   ds->coef = put(p.stage[4], s->coefficients, 2 * s->n_src, st);
-  ds->tgt = put(p.stage[5], s->targets, 2 * s->n_tgt, st);
+  // targets given as the sources array itself: keep them one device array so the
+  // symmetric near tile (every unordered pair once) applies
+  if (s->targets == s->sources && s->n_tgt == s->n_src)
+    ds->tgt = ds->src;
+  else
+    ds->tgt = put(p.stage[5], s->targets, 2 * s->n_tgt, st);
 }
 
 // `load` copies the current host outputs in first (accumulate entry points).
@@ -197,8 +202,11 @@ void check_outputs(const periwave::Periodizer& pz, const pwb::Opts& o, const pwb
   if (k == pwb::Kind::Multipole && !f->complex_scalar) throw std::invalid_argument("complex_scalar output required");
   if (k == pwb::Kind::Velocity && !f->velocity) throw std::invalid_argument("velocity output required");
   if (k == pwb::Kind::Scalar && !f->scalar) throw std::invalid_argument("scalar output required");
-  if (o.with_pressure && !f->pressure) throw std::invalid_argument("pressure output required");
-  if (o.with_gradient && !f->gradient) throw std::invalid_argument("gradient output required");
+  // unsupported combinations are reported by the engine's validation as Unsupported
+  if (o.with_pressure && k == pwb::Kind::Velocity && !pz.dlp && !f->pressure)
+    throw std::invalid_argument("pressure output required");
+  if (o.with_gradient && k == pwb::Kind::Scalar && pz.pde == periwave::Pde::ModHelmholtz && !f->gradient)
+    throw std::invalid_argument("gradient output required");
 }
 
 enum class Mode { Total, Far, Near, Single };

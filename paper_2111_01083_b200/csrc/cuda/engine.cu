@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -595,9 +596,22 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
   a.flag = flag;
   const size_t nout = near_outputs(nk);
-  double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
+  // targets == sources (same array): every unordered pair once (near_sym.cu)
+  const bool symmetric = !single && s.tgt == s.src && s.nt == s.ns && s.nt >= 512 && near_sym_supported(nk) &&
+                         std::getenv("PWB_NO_SYMMETRIC") == nullptr;
   cuda_check(cudaEventRecord(ev_[2], st), "event");
-  launch_near(nk, a, st, ws, sms_);
+  bool done = false;
+  if (symmetric) {
+    const size_t nb = near_sym_tiles(s.nt);
+    auto* fx = sym_fx_.as<unsigned long long>(3 * s.nt * nout);
+    int* rs_dev = sym_rows_.as<int>(nb + 1);
+    int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
+    done = launch_near_sym(nk, a, st, fx, rs_dev, rs_host);
+  }
+  if (!done) {
+    double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
+    launch_near(nk, a, st, ws, sms_);
+  }
   cuda_check(cudaEventRecord(ev_[3], st), "event");
   near_timed_ = true;
   cuda_check(cudaGetLastError(), "near launch");

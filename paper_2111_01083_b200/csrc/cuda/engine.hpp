@@ -130,6 +130,8 @@ class Plan {
   std::vector<std::unique_ptr<Family>> fams_;
   DevBuf s2pw_partial_, coeff_ws_, A_, B_, m0_, near_partial_, flag_, red_m_, red_c_, red_out_;
   PinnedBuf host_checks_;
+  DevBuf sym_fx_, sym_rows_;
+  PinnedBuf sym_rows_host_;
   std::mutex mu_;
   cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
   bool far_timed_ = false, near_timed_ = false;

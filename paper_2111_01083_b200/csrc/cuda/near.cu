@@ -19,17 +19,13 @@
 #include "pw_engine.cuh"
 #include "pw_math.cuh"
 #include "pw_pair.cuh"
+#include "near_common.cuh"
 
 namespace pwb {
 namespace {
 
 constexpr int kThreads = 128;
 constexpr int kTile = 256;
-
-__device__ __forceinline__ bool normal_pos(double p) {
-  const int ex = (pwk::hi_of(p) >> 20) & 0x7ff;
-  return ex != 0 && ex != 0x7ff;
-}
 
 // ---------------------------------------------------------------- pair functors
 // Each functor: NW strength doubles per source, NACC accumulators per target,
@@ -44,7 +40,7 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
       ry2[n] = ry * ry;
     }
     double P = 1.0;
@@ -52,7 +48,7 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
     for (int n = 0; n < NROW; ++n)
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         P *= fma(rx, rx, ry2[n]);
       }
     if (normal_pos(P)) {
@@ -64,8 +60,8 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
     for (int n = 0; n < NROW; ++n)
 #pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
-        const double ry = dy - a.shy[n];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
@@ -86,11 +82,11 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
                                               const NearArgs& a, int& flag) {
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         if (r2 == 0.0) {
           if (rx == 0.0 && ry == 0.0) {
@@ -115,11 +111,11 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
                                               const NearArgs& a, int& flag) {
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         if (r2 == 0.0) {
           if (rx == 0.0 && ry == 0.0) {
@@ -158,12 +154,12 @@ struct Stokes {
     double ax = 0.0, ay = 0.0, pr = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
       const double fy_ry = w[1] * ry;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
         const double t = fma(w[0], rx, fy_ry) * pwk::rcp(r2);
@@ -186,8 +182,8 @@ struct Stokes {
     for (int n = 0; n < NROW; ++n)
 #pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
-        const double ry = dy - a.shy[n];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
@@ -219,10 +215,10 @@ struct ModStokes {
                                               const NearArgs& a, int& flag) {
 #pragma unroll 1
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
 #pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
@@ -256,10 +252,10 @@ struct Stresslet {
                                               const NearArgs& a, int& flag) {
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
@@ -287,10 +283,10 @@ struct Multipole {
                                               const NearArgs& a, int& flag) {
 #pragma unroll 1
     for (int n = 0; n < NROW; ++n) {
-      const double ry = dy - a.shy[n];
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
 #pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
-        const double rx = dx - a.shx[n * NXI + m];
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;

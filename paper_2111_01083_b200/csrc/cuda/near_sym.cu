@@ -1,0 +1,466 @@
+// Symmetric near-image P2P for targets == sources (configs c1, c3, c4, c5).
+//
+// The near image set is symmetric (shift <-> -shift, cell.cpp:47-58), so the
+// image-summed kernel of a pair satisfies G3(t_l - s_j) = +/- G3(t_j - s_l)
+// (even part: log, K0, Stokeslet tensor; odd part: gradient, pressurelet). Each
+// unordered pair is evaluated once and feeds both its row (target l, weight w_j)
+// and its column (target j, weight w_l): half the transcendental work of the
+// one-sided tile (near.cu). Exact-zero semantics are unchanged: an exact zero of
+// (t_l - s_j) - shift is an exact zero of (t_j - s_l) + shift (negation is exact),
+// identity-image self pairs are skipped, any other coincidence sets the flag.
+//
+// Work items: row tile I (256 points, 2 per thread) x a chunk of column tiles
+// J >= I (the diagonal tile runs one-sided). Column partials use a rotating
+// schedule (lane l reads column (l + i) mod 256, one private column copy per
+// warp) so no two lanes of a warp touch the same column and no atomics are needed
+// inside the block. Row and column sums leave the block through integer
+// atomics on a 3-limb fixed-point accumulator (resolution 2^-62, range 2^64):
+// integer addition is associative, so the result is bitwise deterministic for
+// any schedule, and it is converted back to fp64 once at the end.
+#include <cuda_runtime.h>
+
+#include "near_common.cuh"
+#include "pw_engine.cuh"
+#include "pw_math.cuh"
+#include "pw_pair.cuh"
+
+namespace pwb {
+namespace {
+
+constexpr int kT = 128;           // threads per block
+constexpr int kRows = 2 * kT;     // row tile
+constexpr int kCols = 256;        // column tile
+constexpr int kWarps = kT / 32;
+
+// ---------------------------------------------------------------- fixed point
+constexpr double kS0 = 0x1p-22, kS1 = 0x1p20, kS2 = 0x1p62;  // v = a 2^22 + b 2^-20 + c 2^-62
+
+// Limbs truncate toward zero so every limb carries the sign of v and each
+// remainder is exact (it is v minus a same-signed multiple of a power of two).
+__device__ __forceinline__ void fx_add(unsigned long long* base, size_t stride, double v) {
+  const double a = trunc(v * kS0);
+  const double r1 = fma(-a, 0x1p22, v);
+  const double b = trunc(r1 * kS1);
+  const double r2 = fma(-b, 0x1p-20, r1);
+  const double c = rint(r2 * kS2);
+  atomicAdd(base, static_cast<unsigned long long>(static_cast<long long>(a)));
+  atomicAdd(base + stride, static_cast<unsigned long long>(static_cast<long long>(b)));
+  atomicAdd(base + 2 * stride, static_cast<unsigned long long>(static_cast<long long>(c)));
+}
+
+__global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double* out0, int nout0, double* out1,
+                                 int nout1) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int nout = nout0 + nout1;
+  if (i >= n * nout) return;
+  const long long a = static_cast<long long>(acc[i]);
+  const long long b = static_cast<long long>(acc[n * nout + i]);
+  const long long c = static_cast<long long>(acc[2 * n * nout + i]);
+  const double v = fma(static_cast<double>(a), 0x1p22, fma(static_cast<double>(b), 0x1p-20,
+                                                           static_cast<double>(c) * 0x1p-62));
+  const size_t l = i / nout;
+  const int k = static_cast<int>(i % nout);
+  double* dst = k < nout0 ? out0 + l * nout0 + k : out1 + l * nout1 + (k - nout0);
+  *dst += v;
+}
+
+// ---------------------------------------------------------------- symmetric pair values
+// NV image-summed values per pair; row(acc, V, w_j) and col(acc, V, w_l) contract
+// them with the other side's strength (col flips the odd components).
+
+struct SymLaplace {
+  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+    double ry2[NROW];
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
+      ry2[n] = ry * ry;
+    }
+    double P = 1.0;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        P *= fma(rx, rx, ry2[n]);
+      }
+    if (normal_pos(P)) {
+      V[0] = pwk::log_pos(P);
+      return;
+    }
+    double L = 0.0;
+#pragma unroll 1
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll 1
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = row_dy<NXI, NROW>(dy, a, n);
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        L += pwk::log_r2_safe(rx, ry);
+      }
+    V[0] = L;
+  }
+  __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
+    acc[0] = fma(w[0], V[0], acc[0]);
+  }
+  __device__ __forceinline__ static void col(double* acc, const double* V, const double* w) {
+    acc[0] = fma(w[0], V[0], acc[0]);
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    out[0] = acc[0] * (-1.0 / (4.0 * pwk::kPi));
+  }
+};
+
+template <bool GRAD>
+struct SymModHelm {
+  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) V[v] = 0.0;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
+      const double ry2 = ry * ry;
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double r2 = fma(rx, rx, ry2);
+        if (r2 == 0.0) {
+          if (rx == 0.0 && ry == 0.0) {
+            if (n * NXI + m != a.id_img) flag = 1;
+            continue;
+          }
+        }
+        const double X = a.beta2 * r2;
+        if (X < a.xcut2) {
+          if (GRAD) {
+            const pwk::K01 k = pwk::k01_of_sq(X);
+            V[0] += k.k0;
+            V[1] = fma(k.k1_over_x, rx, V[1]);
+            V[2] = fma(k.k1_over_x, ry, V[2]);
+          } else {
+            V[0] += pwk::k0_of_sq(X);
+          }
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = fma(w[0], V[v], acc[v]);
+  }
+  __device__ __forceinline__ static void col(double* acc, const double* V, const double* w) {
+    acc[0] = fma(w[0], V[0], acc[0]);
+    if (GRAD) {  // the gradient kernel is odd in r
+      acc[1] = fma(-w[0], V[1], acc[1]);
+      acc[2] = fma(-w[0], V[2], acc[2]);
+    }
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs& a, double* out) {
+    out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
+    if (GRAD) {
+      const double gs = -a.beta2 / (2.0 * pwk::kPi);
+      out[1] = acc[1] * gs;
+      out[2] = acc[2] * gs;
+    }
+  }
+};
+
+// Stokeslet: V = (log prod r2, Txx, Txy, Tyy [, Px, Py]) with T = sum r r^T / r^2,
+// P = sum r / r^2 (pressurelet, odd).
+template <bool PRESSURE>
+struct SymStokes {
+  static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+    double P = 1.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = row_dy<NXI, NROW>(dy, a, n);
+      const double ry2 = ry * ry;
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double r2 = fma(rx, rx, ry2);
+        P *= r2;
+        const double inv = pwk::rcp(r2);
+        const double xi = rx * inv, yi = ry * inv;
+        txx = fma(xi, rx, txx);
+        txy = fma(xi, ry, txy);
+        tyy = fma(yi, ry, tyy);
+        if (PRESSURE) {
+          px += xi;
+          py += yi;
+        }
+      }
+    }
+    if (normal_pos(P)) {
+      V[0] = pwk::log_pos(P);
+      V[1] = txx;
+      V[2] = txy;
+      V[3] = tyy;
+      if (PRESSURE) {
+        V[4] = px;
+        V[5] = py;
+      }
+      return;
+    }
+    double L = 0.0;
+    txx = txy = tyy = px = py = 0.0;
+#pragma unroll 1
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll 1
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = row_dy<NXI, NROW>(dy, a, n);
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) flag = 1;
+          continue;
+        }
+        const double r2 = fma(rx, rx, ry * ry);
+        L += pwk::log_r2_safe(rx, ry);
+        txx += rx * rx / r2;
+        txy += rx * ry / r2;
+        tyy += ry * ry / r2;
+        px += rx / r2;
+        py += ry / r2;
+      }
+    V[0] = L;
+    V[1] = txx;
+    V[2] = txy;
+    V[3] = tyy;
+    if (PRESSURE) {
+      V[4] = px;
+      V[5] = py;
+    }
+  }
+  // acc = (L fx, L fy, (T f)_x, (T f)_y [, P.f])
+  __device__ __forceinline__ static void contract(double* acc, const double* V, const double* w, double sgn) {
+    acc[0] = fma(V[0], w[0], acc[0]);
+    acc[1] = fma(V[0], w[1], acc[1]);
+    acc[2] = fma(V[1], w[0], fma(V[2], w[1], acc[2]));
+    acc[3] = fma(V[2], w[0], fma(V[3], w[1], acc[3]));
+    if (PRESSURE) acc[4] = fma(sgn * V[4], w[0], fma(sgn * V[5], w[1], acc[4]));
+  }
+  __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
+    contract(acc, V, w, 1.0);
+  }
+  __device__ __forceinline__ static void col(double* acc, const double* V, const double* w) {
+    contract(acc, V, w, -1.0);
+  }
+  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
+    const double c = -1.0 / (4.0 * pwk::kPi);
+    out[0] = c * fma(0.5, acc[0], -acc[2]);
+    out[1] = c * fma(0.5, acc[1], -acc[3]);
+    if (PRESSURE) out[2] = acc[4] * (1.0 / (2.0 * pwk::kPi));
+  }
+};
+
+// ---------------------------------------------------------------- the kernel
+struct SymArgs {
+  NearArgs a;
+  int nb;                      // number of 256-point tiles
+  int chunk;                   // column tiles per work item
+  const int* row_start;        // [nb + 1] first work item of each row tile
+  unsigned long long* fx;      // fixed-point accumulators [3][n][nout]
+};
+
+template <class K>
+__device__ __forceinline__ void load_w(const NearArgs& a, size_t j, bool live, double* w) {
+  if (K::NW == 1) {
+    w[0] = live ? a.q[j] : 0.0;
+  } else {
+    const double2 v = live ? a.vec[j] : make_double2(0.0, 0.0);
+    w[0] = v.x;
+    w[K::NW > 1 ? 1 : 0] = v.y;
+  }
+}
+
+template <class K, int NXI, int NROW>
+__global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
+  const NearArgs& a = S.a;
+  __shared__ double s_x[kCols], s_y[kCols], s_w[K::NW][kCols];
+  __shared__ double s_col[kWarps][K::NACC][kCols];
+
+  // work item -> (row tile I, first column tile)
+  const int item = blockIdx.x;
+  int lo = 0, hi = S.nb;  // find I with row_start[I] <= item < row_start[I+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (S.row_start[mid] <= item) lo = mid; else hi = mid;
+  }
+  const int I = lo;
+  const int J0 = I + (item - S.row_start[I]) * S.chunk;
+  const int J1 = min(S.nb, J0 + S.chunk);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t n = a.nt;
+  double tx[2], ty[2], tw[2][K::NW], racc[2][K::NACC];
+  bool live[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const size_t l = static_cast<size_t>(I) * kRows + tid + k * kT;
+    live[k] = l < n;
+    const double2 p = live[k] ? a.tgt[l] : make_double2(0.0, 0.0);
+    tx[k] = p.x;
+    ty[k] = p.y;
+    load_w<K>(a, l, live[k], tw[k]);
+#pragma unroll
+    for (int c = 0; c < K::NACC; ++c) racc[k][c] = 0.0;
+  }
+  int flag = 0;
+
+  for (int J = J0; J < J1; ++J) {
+    const size_t jbase = static_cast<size_t>(J) * kCols;
+    __syncthreads();
+    for (int i = tid; i < kCols; i += kT) {
+      const size_t j = jbase + i;
+      const bool lv = j < n;
+      const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);  // dead: origin, weight 0
+      s_x[i] = p.x;
+      s_y[i] = p.y;
+      double w[K::NW];
+      load_w<K>(a, j, lv, w);
+#pragma unroll
+      for (int c = 0; c < K::NW; ++c) s_w[c][i] = w[c];
+#pragma unroll
+      for (int c = 0; c < K::NACC; ++c)
+#pragma unroll
+        for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
+    }
+    __syncthreads();
+    if (J == I) {  // diagonal tile: one-sided, every (l, j) once as a row
+      for (int i = 0; i < kCols; ++i) {
+        const double sx = s_x[i], sy = s_y[i];
+        double w[K::NW];
+#pragma unroll
+        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][i];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          double V[K::NV];
+          K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
+          K::row(racc[k], V, w);
+        }
+      }
+      continue;
+    }
+#pragma unroll 1
+    for (int i = 0; i < kCols; ++i) {
+      const int jj = (lane + i) & (kCols - 1);
+      const double sx = s_x[jj], sy = s_y[jj];
+      double w[K::NW];
+#pragma unroll
+      for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+      double cacc[K::NACC];
+#pragma unroll
+      for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        double V[K::NV];
+        // (t - s) - shift as upstream (apply.cpp:534)
+        K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
+        K::row(racc[k], V, w);
+        K::col(cacc, V, tw[k]);
+      }
+#pragma unroll
+      for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+    }
+    __syncthreads();
+    // column totals of this tile -> fixed point
+    for (int i = tid; i < kCols; i += kT) {
+      const size_t j = jbase + i;
+      if (j >= n) continue;
+      double acc[K::NACC];
+#pragma unroll
+      for (int c = 0; c < K::NACC; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int wv = 0; wv < kWarps; ++wv) s += s_col[wv][c][i];
+        acc[c] = s;
+      }
+      double o[K::NOUT];
+      K::finish(acc, a, o);
+#pragma unroll
+      for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + j * K::NOUT + c, n * K::NOUT, o[c]);
+    }
+  }
+  if (flag) atomicOr(a.flag, 1);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (!live[k]) continue;
+    const size_t l = static_cast<size_t>(I) * kRows + tid + k * kT;
+    double o[K::NOUT];
+    K::finish(racc[k], a, o);
+#pragma unroll
+    for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + l * K::NOUT + c, n * K::NOUT, o[c]);
+  }
+}
+
+template <class K, int NXI, int NROW>
+void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
+                      int* row_start_host, int chunk) {
+  static_assert(kRows == kCols, "row and column tiles must match");
+  const int nb = static_cast<int>((a.nt + kCols - 1) / kCols);
+  int items = 0;
+  for (int I = 0; I < nb; ++I) {
+    row_start_host[I] = items;
+    items += (nb - I + chunk - 1) / chunk;
+  }
+  row_start_host[nb] = items;
+  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+             "row starts");
+  const size_t nout = K::NOUT;
+  cuda_check(cudaMemsetAsync(fx, 0, 3 * a.nt * nout * sizeof(unsigned long long), st), "memset fx");
+  SymArgs S;
+  S.a = a;
+  S.nb = nb;
+  S.chunk = chunk;
+  S.row_start = row_start_dev;
+  S.fx = fx;
+  near_sym_kernel<K, NXI, NROW><<<items, kT, 0, st>>>(S);
+  const size_t total = a.nt * nout;
+  fx_finish_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(fx, a.nt, a.out0, a.nout0, a.out1,
+                                                                              a.nout1);
+  count_launches(2);
+}
+
+template <class K>
+bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh, int chunk) {
+  if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh, chunk), true;
+  if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh, chunk), true;
+  if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh, chunk), true;
+  if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh, chunk), true;
+  return false;
+}
+
+}  // namespace
+
+size_t near_sym_tiles(size_t n) { return (n + kCols - 1) / kCols; }
+
+bool near_sym_supported(NearKind kind) {
+  return kind == NearKind::Laplace || kind == NearKind::ModHelm || kind == NearKind::ModHelmGrad ||
+         kind == NearKind::Stokes || kind == NearKind::StokesP;
+}
+
+bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
+                     int* row_start_host) {
+  if (a.nt == 0) return true;
+  const int chunk = 16;
+  switch (kind) {
+    case NearKind::Laplace: return dispatch_sym<SymLaplace>(a, st, fx, row_start_dev, row_start_host, chunk);
+    case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, row_start_dev, row_start_host, chunk);
+    case NearKind::ModHelmGrad:
+      return dispatch_sym<SymModHelm<true>>(a, st, fx, row_start_dev, row_start_host, chunk);
+    case NearKind::Stokes: return dispatch_sym<SymStokes<false>>(a, st, fx, row_start_dev, row_start_host, chunk);
+    case NearKind::StokesP: return dispatch_sym<SymStokes<true>>(a, st, fx, row_start_dev, row_start_host, chunk);
+    default: return false;
+  }
+}
+
+}  // namespace pwb

@@ -54,6 +54,13 @@ struct NearArgs {
 
 size_t near_outputs(NearKind kind);
 void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count);
+// Symmetric (targets == sources) fused near images: each unordered pair once
+// (near_sym.cu). fx: 3 * n * nout uint64 accumulators; row_start: nb + 1 ints
+// (device and pinned host). Returns false when the kind/layout has no symmetric form.
+bool near_sym_supported(NearKind kind);
+size_t near_sym_tiles(size_t n);
+bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
+                     int* row_start_host);
 
 // ---------------------------------------------------------------- far field (direct S2PW / PW2T)
 // Weight sets: what each source contributes per mode (K real weights).
