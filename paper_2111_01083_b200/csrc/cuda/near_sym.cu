@@ -9,14 +9,21 @@
 // (t_l - s_j) - shift is an exact zero of (t_j - s_l) + shift (negation is exact),
 // identity-image self pairs are skipped, any other coincidence sets the flag.
 //
-// Work items: row tile I (256 points, 2 per thread) x a chunk of column tiles
-// J >= I (the diagonal tile runs one-sided). Column partials use a rotating
-// schedule (lane l reads column (l + i) mod 256, one private column copy per
-// warp) so no two lanes of a warp touch the same column and no atomics are needed
-// inside the block. Row and column sums leave the block through integer
-// atomics on a 3-limb fixed-point accumulator (resolution 2^-62, range 2^64):
-// integer addition is associative, so the result is bitwise deterministic for
-// any schedule, and it is converted back to fp64 once at the end.
+// Work items: row tile I (TILE = 128 * TPT points, TPT per thread) x a chunk of
+// column tiles J >= I (the diagonal tile runs one-sided). Column partials use a
+// rotating schedule (lane l reads column (l + i) mod TILE, one private column
+// copy per warp) so no two lanes of a warp touch the same column and no atomics
+// are needed inside the block.
+//
+// Fast path: for kernels whose per-pair work is a product of image distances
+// (Laplace log, Stokeslet) the off-diagonal tiles run branch-free; a pair whose
+// product is 0 / subnormal / inf (exact coincidence, extreme scales) only raises
+// a flag, and a tile that saw one is redone on the careful per-image path.
+//
+// Row and column sums leave the block through integer atomics on a 3-limb
+// fixed-point accumulator (resolution 2^-62, range 2^64): integer addition is
+// associative, so the result is bitwise deterministic for any schedule, and it
+// is converted back to fp64 once at the end.
 #include <cuda_runtime.h>
 
 #include "near_common.cuh"
@@ -27,22 +34,18 @@
 namespace pwb {
 namespace {
 
-constexpr int kT = 128;           // threads per block
-constexpr int kRows = 2 * kT;     // row tile
-constexpr int kCols = 256;        // column tile
+constexpr int kT = 128;  // threads per block
 constexpr int kWarps = kT / 32;
 
 // ---------------------------------------------------------------- fixed point
-constexpr double kS0 = 0x1p-22, kS1 = 0x1p20, kS2 = 0x1p62;  // v = a 2^22 + b 2^-20 + c 2^-62
-
-// Limbs truncate toward zero so every limb carries the sign of v and each
-// remainder is exact (it is v minus a same-signed multiple of a power of two).
+// v = a 2^22 + b 2^-20 + c 2^-62; limbs truncate toward zero so each carries the
+// sign of v and each remainder is exact.
 __device__ __forceinline__ void fx_add(unsigned long long* base, size_t stride, double v) {
-  const double a = trunc(v * kS0);
+  const double a = trunc(v * 0x1p-22);
   const double r1 = fma(-a, 0x1p22, v);
-  const double b = trunc(r1 * kS1);
+  const double b = trunc(r1 * 0x1p20);
   const double r2 = fma(-b, 0x1p-20, r1);
-  const double c = rint(r2 * kS2);
+  const double c = rint(r2 * 0x1p62);
   atomicAdd(base, static_cast<unsigned long long>(static_cast<long long>(a)));
   atomicAdd(base + stride, static_cast<unsigned long long>(static_cast<long long>(b)));
   atomicAdd(base + 2 * stride, static_cast<unsigned long long>(static_cast<long long>(c)));
@@ -56,8 +59,8 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
   const long long a = static_cast<long long>(acc[i]);
   const long long b = static_cast<long long>(acc[n * nout + i]);
   const long long c = static_cast<long long>(acc[2 * n * nout + i]);
-  const double v = fma(static_cast<double>(a), 0x1p22, fma(static_cast<double>(b), 0x1p-20,
-                                                           static_cast<double>(c) * 0x1p-62));
+  const double v = fma(static_cast<double>(a), 0x1p22,
+                       fma(static_cast<double>(b), 0x1p-20, static_cast<double>(c) * 0x1p-62));
   const size_t l = i / nout;
   const int k = static_cast<int>(i % nout);
   double* dst = k < nout0 ? out0 + l * nout0 + k : out1 + l * nout1 + (k - nout0);
@@ -67,11 +70,15 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
 // ---------------------------------------------------------------- symmetric pair values
 // NV image-summed values per pair; row(acc, V, w_j) and col(acc, V, w_l) contract
 // them with the other side's strength (col flips the odd components).
+// values():      careful per-image semantics (slow path included, sets `flag`);
+// values_fast(): branch-free, only valid when `bad` stays 0 (FAST kernels).
 
 struct SymLaplace {
-  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1;
+  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = 4, CHUNK = 8;
+  static constexpr bool FAST = true;
   template <int NXI, int NROW>
-  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+  __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
+                                                     const pwk::LogK& K, int& bad) {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -86,14 +93,12 @@ struct SymLaplace {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         P *= fma(rx, rx, ry2[n]);
       }
-    if (normal_pos(P)) {
-      V[0] = pwk::log_pos(P);
-      return;
-    }
+    V[0] = pwk::log_pos_k(P, K, bad);
+  }
+  template <int NXI, int NROW>
+  __device__ __noinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
     double L = 0.0;
-#pragma unroll 1
     for (int n = 0; n < NROW; ++n)
-#pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double ry = row_dy<NXI, NROW>(dy, a, n);
@@ -118,7 +123,11 @@ struct SymLaplace {
 
 template <bool GRAD>
 struct SymModHelm {
-  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV;
+  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16;
+  static constexpr bool FAST = false;
+  template <int NXI, int NROW>
+  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const pwk::LogK&,
+                                                     int&) {}
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
 #pragma unroll
@@ -176,9 +185,12 @@ struct SymModHelm {
 // P = sum r / r^2 (pressurelet, odd).
 template <bool PRESSURE>
 struct SymStokes {
-  static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2;
+  static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
+                       CHUNK = 16;
+  static constexpr bool FAST = true;
   template <int NXI, int NROW>
-  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+  __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
+                                                     const pwk::LogK& K, int& bad) {
     double P = 1.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -200,22 +212,19 @@ struct SymStokes {
         }
       }
     }
-    if (normal_pos(P)) {
-      V[0] = pwk::log_pos(P);
-      V[1] = txx;
-      V[2] = txy;
-      V[3] = tyy;
-      if (PRESSURE) {
-        V[4] = px;
-        V[5] = py;
-      }
-      return;
+    V[0] = pwk::log_pos_k(P, K, bad);
+    V[1] = txx;
+    V[2] = txy;
+    V[3] = tyy;
+    if (PRESSURE) {
+      V[4] = px;
+      V[5] = py;
     }
-    double L = 0.0;
-    txx = txy = tyy = px = py = 0.0;
-#pragma unroll 1
+  }
+  template <int NXI, int NROW>
+  __device__ __noinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+    double L = 0.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
     for (int n = 0; n < NROW; ++n)
-#pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double ry = row_dy<NXI, NROW>(dy, a, n);
@@ -265,10 +274,10 @@ struct SymStokes {
 // ---------------------------------------------------------------- the kernel
 struct SymArgs {
   NearArgs a;
-  int nb;                      // number of 256-point tiles
-  int chunk;                   // column tiles per work item
-  const int* row_start;        // [nb + 1] first work item of each row tile
-  unsigned long long* fx;      // fixed-point accumulators [3][n][nout]
+  int nb;                  // number of TILE-point tiles
+  int chunk;               // column tiles per work item
+  const int* row_start;    // [nb + 1] first work item of each row tile
+  unsigned long long* fx;  // fixed-point accumulators [3][n][nout]
 };
 
 template <class K>
@@ -284,16 +293,21 @@ __device__ __forceinline__ void load_w(const NearArgs& a, size_t j, bool live, d
 
 template <class K, int NXI, int NROW>
 __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
+  constexpr int TPT = K::TPT;
+  constexpr int TILE = kT * TPT;
   const NearArgs& a = S.a;
-  __shared__ double s_x[kCols], s_y[kCols], s_w[K::NW][kCols];
-  __shared__ double s_col[kWarps][K::NACC][kCols];
+  __shared__ double s_x[TILE], s_y[TILE], s_w[K::NW][TILE];
+  __shared__ double s_col[kWarps][K::NACC][TILE];
 
   // work item -> (row tile I, first column tile)
   const int item = blockIdx.x;
-  int lo = 0, hi = S.nb;  // find I with row_start[I] <= item < row_start[I+1]
+  int lo = 0, hi = S.nb;  // row_start[I] <= item < row_start[I+1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (S.row_start[mid] <= item) lo = mid; else hi = mid;
+    if (S.row_start[mid] <= item)
+      lo = mid;
+    else
+      hi = mid;
   }
   const int I = lo;
   const int J0 = I + (item - S.row_start[I]) * S.chunk;
@@ -301,13 +315,13 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t n = a.nt;
-  double tx[2], ty[2], tw[2][K::NW], racc[2][K::NACC];
-  bool live[2];
+  double tx[TPT], ty[TPT], tw[TPT][K::NW], racc[TPT][K::NACC];
+  bool live[TPT];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const size_t l = static_cast<size_t>(I) * kRows + tid + k * kT;
+  for (int k = 0; k < TPT; ++k) {
+    const size_t l = static_cast<size_t>(I) * TILE + tid + k * kT;
     live[k] = l < n;
-    const double2 p = live[k] ? a.tgt[l] : make_double2(0.0, 0.0);
+    const double2 p = live[k] ? a.tgt[l] : make_double2(0.0, 0.0);  // dead: origin, weight 0
     tx[k] = p.x;
     ty[k] = p.y;
     load_w<K>(a, l, live[k], tw[k]);
@@ -315,14 +329,16 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
     for (int c = 0; c < K::NACC; ++c) racc[k][c] = 0.0;
   }
   int flag = 0;
+  pwk::LogK LK;
+  if (K::FAST) LK = pwk::log_consts();
 
   for (int J = J0; J < J1; ++J) {
-    const size_t jbase = static_cast<size_t>(J) * kCols;
+    const size_t jbase = static_cast<size_t>(J) * TILE;
     __syncthreads();
-    for (int i = tid; i < kCols; i += kT) {
+    for (int i = tid; i < TILE; i += kT) {
       const size_t j = jbase + i;
       const bool lv = j < n;
-      const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);  // dead: origin, weight 0
+      const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);
       s_x[i] = p.x;
       s_y[i] = p.y;
       double w[K::NW];
@@ -335,14 +351,14 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
         for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
     }
     __syncthreads();
-    if (J == I) {  // diagonal tile: one-sided, every (l, j) once as a row
-      for (int i = 0; i < kCols; ++i) {
+    if (J == I) {  // diagonal tile: one-sided and careful (self pairs live here)
+      for (int i = 0; i < TILE; ++i) {
         const double sx = s_x[i], sy = s_y[i];
         double w[K::NW];
 #pragma unroll
         for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][i];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < TPT; ++k) {
           double V[K::NV];
           K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
           K::row(racc[k], V, w);
@@ -350,30 +366,74 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
       }
       continue;
     }
-#pragma unroll 1
-    for (int i = 0; i < kCols; ++i) {
-      const int jj = (lane + i) & (kCols - 1);
-      const double sx = s_x[jj], sy = s_y[jj];
-      double w[K::NW];
+    bool careful = !K::FAST;
+    if (K::FAST) {
+      double keep[TPT][K::NACC];
 #pragma unroll
-      for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
-      double cacc[K::NACC];
+      for (int k = 0; k < TPT; ++k)
 #pragma unroll
-      for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+        for (int c = 0; c < K::NACC; ++c) keep[k][c] = racc[k][c];
+      int bad = 0;
+#pragma unroll 2
+      for (int i = 0; i < TILE; ++i) {
+        const int jj = (lane + i) & (TILE - 1);
+        const double sx = s_x[jj], sy = s_y[jj];
+        double w[K::NW];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        double V[K::NV];
-        // (t - s) - shift as upstream (apply.cpp:534)
-        K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
-        K::row(racc[k], V, w);
-        K::col(cacc, V, tw[k]);
+        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+        double cacc[K::NACC];
+#pragma unroll
+        for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          double V[K::NV];
+          // (t - s) - shift as upstream (apply.cpp:534)
+          K::template values_fast<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
+          K::row(racc[k], V, w);
+          K::col(cacc, V, tw[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
       }
+      if (__syncthreads_or(bad)) {  // rare: redo this tile on the careful path
 #pragma unroll
-      for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+        for (int k = 0; k < TPT; ++k)
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c) racc[k][c] = keep[k][c];
+        for (int i = tid; i < TILE; i += kT)
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c)
+#pragma unroll
+            for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
+        __syncthreads();
+        careful = true;
+      }
+    }
+    if (careful) {
+#pragma unroll 1
+      for (int i = 0; i < TILE; ++i) {
+        const int jj = (lane + i) & (TILE - 1);
+        const double sx = s_x[jj], sy = s_y[jj];
+        double w[K::NW];
+#pragma unroll
+        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+        double cacc[K::NACC];
+#pragma unroll
+        for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          double V[K::NV];
+          K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
+          K::row(racc[k], V, w);
+          K::col(cacc, V, tw[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+      }
     }
     __syncthreads();
     // column totals of this tile -> fixed point
-    for (int i = tid; i < kCols; i += kT) {
+    for (int i = tid; i < TILE; i += kT) {
       const size_t j = jbase + i;
       if (j >= n) continue;
       double acc[K::NACC];
@@ -392,9 +452,9 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
   }
   if (flag) atomicOr(a.flag, 1);
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < TPT; ++k) {
     if (!live[k]) continue;
-    const size_t l = static_cast<size_t>(I) * kRows + tid + k * kT;
+    const size_t l = static_cast<size_t>(I) * TILE + tid + k * kT;
     double o[K::NOUT];
     K::finish(racc[k], a, o);
 #pragma unroll
@@ -404,9 +464,10 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
 
 template <class K, int NXI, int NROW>
 void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                      int* row_start_host, int chunk) {
-  static_assert(kRows == kCols, "row and column tiles must match");
-  const int nb = static_cast<int>((a.nt + kCols - 1) / kCols);
+                      int* row_start_host) {
+  constexpr int TILE = kT * K::TPT;
+  const int chunk = K::CHUNK;
+  const int nb = static_cast<int>((a.nt + TILE - 1) / TILE);
   int items = 0;
   for (int I = 0; I < nb; ++I) {
     row_start_host[I] = items;
@@ -431,17 +492,18 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
 }
 
 template <class K>
-bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh, int chunk) {
-  if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh, chunk), true;
-  if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh, chunk), true;
-  if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh, chunk), true;
-  if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh, chunk), true;
+bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh) {
+  if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh), true;
+  if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh), true;
+  if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh), true;
+  if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh), true;
   return false;
 }
 
 }  // namespace
 
-size_t near_sym_tiles(size_t n) { return (n + kCols - 1) / kCols; }
+// upper bound on the number of tiles (the smallest tile is 256 points)
+size_t near_sym_tiles(size_t n) { return (n + 255) / 256; }
 
 bool near_sym_supported(NearKind kind) {
   return kind == NearKind::Laplace || kind == NearKind::ModHelm || kind == NearKind::ModHelmGrad ||
@@ -451,14 +513,12 @@ bool near_sym_supported(NearKind kind) {
 bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
                      int* row_start_host) {
   if (a.nt == 0) return true;
-  const int chunk = 16;
   switch (kind) {
-    case NearKind::Laplace: return dispatch_sym<SymLaplace>(a, st, fx, row_start_dev, row_start_host, chunk);
-    case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, row_start_dev, row_start_host, chunk);
-    case NearKind::ModHelmGrad:
-      return dispatch_sym<SymModHelm<true>>(a, st, fx, row_start_dev, row_start_host, chunk);
-    case NearKind::Stokes: return dispatch_sym<SymStokes<false>>(a, st, fx, row_start_dev, row_start_host, chunk);
-    case NearKind::StokesP: return dispatch_sym<SymStokes<true>>(a, st, fx, row_start_dev, row_start_host, chunk);
+    case NearKind::Laplace: return dispatch_sym<SymLaplace>(a, st, fx, row_start_dev, row_start_host);
+    case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, row_start_dev, row_start_host);
+    case NearKind::ModHelmGrad: return dispatch_sym<SymModHelm<true>>(a, st, fx, row_start_dev, row_start_host);
+    case NearKind::Stokes: return dispatch_sym<SymStokes<false>>(a, st, fx, row_start_dev, row_start_host);
+    case NearKind::StokesP: return dispatch_sym<SymStokes<true>>(a, st, fx, row_start_dev, row_start_host);
     default: return false;
   }
 }

@@ -338,7 +338,7 @@ def test_symmetric_targets_equal_sources(pw, gpu, ref, name, n):
                   key)
     again = getattr(pw.total_field(pz, pw.ParticleSystem(sources=inp.sources, targets=inp.sources, **kw), opt), key)
     assert np.array_equal(sym, again)  # fixed-point accumulation: bitwise deterministic
-    assert rel_l2(sym, one) <= 1e-14
+    assert rel_l2(sym, one) <= 1e-13
     R = ref.make_periodizer(int(c.pde), c.beta, tuple(float(v) for v in c.cell[:3]) + (int(c.cell[3]),), c.eps)
     idx = inp.sample[:300]
     want = R.apply(0, inp.sources, np.ascontiguousarray(inp.sources[idx]), path=1, threads=8, **kw)[key]
