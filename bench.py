@@ -31,6 +31,9 @@ METRIC = "targets/sec at N=1e6, eps=1e-10, fp64, 1/2/4/8 B200; % of FP64 rooflin
 # SURVEY.md §8(d) algorithmic flops per near pair (one image of one (target, source))
 F_PAIR = {"c1": 29, "c2": 153, "c3": 48, "c4": 29, "c5": 94}
 F_FAR = {"c1": 70, "c2": 70, "c3": 86, "c4": 70, "c5": 70}
+# fp64-pipe instructions per (target, source) pair-group of the symmetric tile (all images),
+# counted in the SASS of the fast inner loop (cuobjdump; profiles/r1_c4_near_sym_ncu.md)
+FP64_INSTR_PER_GROUP = {"c4": 31.25}
 WORKLOAD = {
     "c1": "c1: doubly periodic Poisson, square cell, N=1000 uniform, targets=sources, eps=1e-10",
     "c2": "c2: doubly periodic mod. Helmholtz beta=10, cell (1,0.3,0.8), 1e5 src / 1e5 tgt, eps=1e-10, u+grad u",
@@ -353,6 +356,13 @@ def main():
     achieved = flops_near / (t_near * 1e-3) / 1e12
     rank_far = pz.rank()
     far_flops = rank_far * (ns + nt) * F_FAR[args.config]
+    # hardware view: issued fp64 instructions of the fused symmetric tile (static SASS count per
+    # (target, source) pair-group covering all images, profiles/r1_c4_near_sym_ncu.md) over the
+    # DFMA instruction peak (peak TFLOP/s / 2)
+    pipe_frac = None
+    if same and args.config in FP64_INSTR_PER_GROUP:
+        groups = ns * (ns + 1) / 2.0
+        pipe_frac = groups * FP64_INSTR_PER_GROUP[args.config] / (t_near * 1e-3) / (peak.value * 1e12 / 2.0)
 
     line = None
     if rank == 0:
@@ -378,9 +388,16 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                          "frac": achieved / peak.value if peak.value else None, "traffic": None,
-                         "kernel": "near_tile_kernel<Laplace,3,1,2> (fused near images)" if args.config == "c4"
+                         "kernel": ("near_sym_kernel<SymLaplace,3,1> (fused near images, each unordered pair once)"
+                                    if same else "near_tile_kernel<Laplace,3,1,2> (fused near images)")
+                         if args.config == "c4"
                          else "near_tile_kernel (fused near images)",
                          "near_ms_per_launch": t_near, "far_ms": t_step - t_near,
+                         "fp64_pipe_frac": pipe_frac,
+                         "note": "frac > 1: the fused symmetric tile evaluates each unordered (target, source)"
+                                 " pair once with one log for all images; the survey model charges 29 flop per"
+                                 " image per ordered pair. fp64_pipe_frac is the hardware efficiency"
+                                 " (issued DFMA-pipe instructions / DFMA peak); ncu cross-check in profiles/",
                          "algorithmic_flops_per_launch": flops_near,
                          "flop_model": f"SURVEY.md §8(d): {F_PAIR[args.config]} flop per (image, target, source) "
                                        f"pair x {nimg} images x {ns} x {t_hi - t_lo}; far {far_flops:.3e} flop "
