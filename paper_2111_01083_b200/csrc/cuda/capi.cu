@@ -599,17 +599,22 @@ int pwb_choose_path(const pwb_periodizer* pz, size_t n_src, size_t n_tgt, int* p
   });
 }
 
-int pwb_far_coeff_size(const pwb_periodizer* h, const pwb_options* o, size_t, size_t, size_t* n) {
+int pwb_far_coeff_size(const pwb_periodizer* h, const pwb_options* o, size_t ns_total, size_t nt_total, size_t* n) {
   if (!h || !n) return fail_arg("null argument");
   return guard([&] {
     const int dev = current_device(o ? o->device : -1);
-    *n = const_cast<pwb_periodizer*>(h)->plan(dev).coeff_size(opts_from(o));
+    pwb::Plan& p = const_cast<pwb_periodizer*>(h)->plan(dev);
+    std::lock_guard<std::mutex> lock(p.mutex());
+    const pwb::Opts opt = opts_from(o);
+    *n = p.coeff_size(opt, p.resolve(opt, ns_total, nt_total));
     return OK;
   });
 }
 
-int pwb_far_source_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, size_t, size_t,
-                        double* coeff) {
+// The path of a sharded apply is resolved from the global counts (choose_path,
+// apply.cpp:409-415); 0 means "this shard is the whole problem".
+int pwb_far_source_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, size_t ns_total,
+                        size_t nt_total, double* coeff) {
   if (!h || !s || !coeff) return fail_arg("null argument");
   if (s->memory != PWB_MEM_DEVICE) return fail_arg("sharded passes take device memory");
   return guard([&] {
@@ -619,16 +624,18 @@ int pwb_far_source_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_
     pwb::Opts opt = opts_from(o);
     pwb::DevSys ds;
     stage_in(p, s, p.stream_for(opt), &ds);
+    const size_t nt_local = ds.nt;
     ds.nt = 0;
     p.validate(ds, opt, true, /*neutrality=*/false);  // neutrality is a property of the global system
-    p.source_pass(ds, opt, coeff);
+    const auto path = p.resolve(opt, ns_total ? ns_total : s->n_src, nt_total ? nt_total : nt_local);
+    p.source_pass(ds, opt, coeff, path);
     pwb::cuda_check(cudaStreamSynchronize(p.stream_for(opt)), "sync");
     return OK;
   });
 }
 
-int pwb_far_target_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, size_t, size_t,
-                        const double* coeff, pwb_field* f) {
+int pwb_far_target_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, size_t ns_total,
+                        size_t nt_total, const double* coeff, pwb_field* f) {
   if (!h || !s || !coeff || !f) return fail_arg("null argument");
   if (s->memory != PWB_MEM_DEVICE || f->memory != PWB_MEM_DEVICE) return fail_arg("sharded passes take device memory");
   return guard([&] {
@@ -640,9 +647,9 @@ int pwb_far_target_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_
     stage_in(p, s, p.stream_for(opt), &ds);
     pwb::DevOut dout;
     stage_out(p, f, s->n_tgt, p.stream_for(opt), false, &dout);
-    p.target_pass(ds, opt, coeff, dout);
+    const auto path = p.resolve(opt, ns_total ? ns_total : s->n_src, nt_total ? nt_total : s->n_tgt);
+    f->accelerated = p.target_pass(ds, opt, coeff, dout, path) ? 1 : 0;
     pwb::cuda_check(cudaStreamSynchronize(p.stream_for(opt)), "sync");
-    f->accelerated = 0;
     return OK;
   });
 }
@@ -676,7 +683,7 @@ int pwb_nufft_type3(int backend, double eps, size_t n, const double* x, const do
   return guard([&] { return pwb::nufft_entry(3, backend, eps, n, x, c, nk, s, f, memory, stream); });
 }
 
-int pwb_fast_nufft_available(void) { return 0; }  // accelerated backend not yet built
+int pwb_fast_nufft_available(void) { return 1; }
 
 int pwb_eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out) {
   if (which < 0 || which > 5) return fail_arg("unknown kernel");

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "engine.hpp"
+#include "nufft.hpp"
 
 namespace pwb {
 
@@ -167,33 +168,42 @@ void Plan::phase_ms(double* far_ms, double* near_ms) {
 void Plan::build_families() {
   const Kind kind = kind_of(pz_);
   if (kind != Kind::Velocity) {
-    auto f = std::make_unique<Family>();
-    f->kind = FamilyKind::Scalar;
-    f->ws = kind == Kind::Multipole ? WeightSet::Coef : WeightSet::Charge;
-    f->ko = 1;
-    HostModes hm;
-    std::vector<double> diag;
-    double m0sum = 0.0;
-    bool any_m0 = false;
-    for (const auto& p : pz_.scalar_parts) {
-      require(p.diag.size() == p.modes.size(), ErrorCode::LengthMismatch, "scalar part diag/mode size mismatch");
-      require_vertical_m0(p.modes, p.has_m0);
-      hm.add(p.modes);
-      for (const auto& c : p.diag) push_c(diag, c);
-      if (p.has_m0) {
-        any_m0 = true;
-        m0sum += p.m0_coef;
+    // two scalar families: vertical parts (S, N; the accelerated route is the type-1/2
+    // NUFFT, apply.cpp:200-259) and horizontal parts (W, E; type 3 on strips, :269-348)
+    for (int axis = 0; axis < 2; ++axis) {
+      auto f = std::make_unique<Family>();
+      f->kind = FamilyKind::Scalar;
+      f->ws = kind == Kind::Multipole ? WeightSet::Coef : WeightSet::Charge;
+      f->ko = 1;
+      f->axis_group = axis;
+      HostModes hm;
+      std::vector<double> diag;
+      double m0sum = 0.0;
+      bool any_m0 = false;
+      for (const auto& p : pz_.scalar_parts) {
+        require(p.diag.size() == p.modes.size(), ErrorCode::LengthMismatch, "scalar part diag/mode size mismatch");
+        require_vertical_m0(p.modes, p.has_m0);
+        const int pa = p.modes.axis == periwave::Axis::Horizontal ? 1 : 0;
+        if (pa != axis) continue;
+        hm.add(p.modes);
+        f->part_sizes.push_back(static_cast<int>(p.modes.size()));
+        for (const auto& c : p.diag) push_c(diag, c);
+        if (p.has_m0) {
+          any_m0 = true;
+          m0sum += p.m0_coef;
+        }
       }
+      hm.to(*f);
+      upload(f->t[0], diag);
+      f->host_phase = hm.phase;
+      if (any_m0 && kind == Kind::Scalar) {
+        f->has_lin = true;
+        f->ia = 0;
+        f->ib = 0;
+        f->mlin[0] = m0sum;
+      }
+      fams_.push_back(std::move(f));
     }
-    hm.to(*f);
-    upload(f->t[0], diag);
-    if (any_m0 && kind == Kind::Scalar) {
-      f->has_lin = true;
-      f->ia = 0;
-      f->ib = 0;
-      f->mlin[0] = m0sum;
-    }
-    fams_.push_back(std::move(f));
     return;
   }
   if (!pz_.block_parts.empty()) {
@@ -332,11 +342,143 @@ int Plan::s2pw_chunks(size_t ns, int modes, int k) const {
   return static_cast<int>(std::max(1L, std::min(want, 1024L)));
 }
 
-size_t Plan::coeff_size(const Opts& o) const {
+periwave::ApplyPath Plan::resolve(const Opts& o, size_t n_src_total, size_t n_tgt_total) const {
+  if (o.path != periwave::ApplyPath::Auto) return o.path;
+  return periwave::choose_path(pz_, n_src_total, n_tgt_total);
+}
+
+bool Plan::vert_accel(const Family& f, const Opts& o, periwave::ApplyPath path) const {
+  // the gradient extension needs per-mode derivative symbols: it stays on the direct sweep
+  return path == periwave::ApplyPath::Accelerated && f.kind == FamilyKind::Scalar && f.axis_group == 0 &&
+         f.count > 0 && !o.with_gradient;
+}
+
+bool Plan::horiz_accel(const Family& f, const Opts& o, periwave::ApplyPath path) const {
+  // apply.cpp:456-458: the west/east parts accelerate on singly periodic cells only
+  return path == periwave::ApplyPath::Accelerated && f.kind == FamilyKind::Scalar && f.axis_group == 1 &&
+         f.count > 0 && pz_.cell.periodicity == periwave::Periodicity::Singly && !o.with_gradient;
+}
+
+void Plan::ensure_horiz_accel(double eps) {
+  const Family& f = *fams_[1];
+  const periwave::UnitCell& c = pz_.cell;
+  if (!ha_.ready) {
+    // interval of the closed cell in x (cell.cpp:66-70 slack) instead of the data span of
+    // apply.cpp:275-285: covers every admissible point, and is the same on every rank
+    const double ext = (0.5 + 1e-12) * (c.d + std::abs(c.xi));
+    ha_.lo = -ext;
+    ha_.hi = ext;
+    ha_.ymax = (0.5 + 1e-12) * c.eta;
+    const double width = ha_.hi - ha_.lo;
+    const double margin = 2.0 * c.d - width;  // > 0: |xi| <= d/2 on strips
+    const double e = std::max(pz_.eps, 1e-14);
+    const double u = 1.0 + 2.0 * margin / width;
+    const double rho = u + std::sqrt(u * u - 1.0);
+    ha_.mg = std::clamp(static_cast<int>(std::ceil(std::log(1.0 / e) / std::log(rho))) + 2, 4, 64);  // apply.cpp:290
+    const periwave::BarycentricGrid g = periwave::make_barycentric_grid(ha_.lo, ha_.hi, ha_.mg);
+    for (int k = 0; k < ha_.mg; ++k) {
+      ha_.tk[k] = (2.0 * g.nodes[k] - g.lo - g.hi) / (g.hi - g.lo);
+      ha_.bw[k] = g.bary_w[k];
+    }
+    upload(ha_.nodes, g.nodes);
+    std::vector<double> neg(f.host_phase.size());
+    ha_.lmax = 0.0;
+    for (size_t r = 0; r < neg.size(); ++r) {
+      neg[r] = -f.host_phase[r];
+      ha_.lmax = std::max(ha_.lmax, std::abs(f.host_phase[r]));
+    }
+    upload(ha_.neg_lam, neg);
+    ha_.part_start.assign(1, 0);
+    for (int sz : f.part_sizes) ha_.part_start.push_back(ha_.part_start.back() + sz);
+    ha_.ready = true;
+  }
+  if (ha_.eps != eps) {
+    const EsSpec s = es_spec(eps);
+    ha_.w = s.w;
+    ha_.beta = s.beta;
+    // source side: x = y_j, s = -lambda (nufft_fast.cpp:505-507)
+    ha_.hx1 = periwave::kPi / (2.0 * ha_.lmax);
+    ha_.nf1 = static_cast<int>(next_fast_even(2 * static_cast<size_t>(std::ceil(ha_.ymax / ha_.hx1)) + 2 * s.w + 4));
+    std::vector<double> fac(f.host_phase.size());
+    for (size_t r = 0; r < fac.size(); ++r)
+      fac[r] = (2.0 / s.w) / phihat(s, -f.host_phase[r] * 0.5 * s.w * ha_.hx1);
+    upload(ha_.fac1, fac);
+    // target side: x = lambda_r, s = y_l
+    ha_.hx2 = periwave::kPi / (2.0 * ha_.ymax);
+    ha_.nf2 = static_cast<int>(next_fast_even(2 * static_cast<size_t>(std::ceil(ha_.lmax / ha_.hx2)) + 2 * s.w + 4));
+    require(ha_.nf1 <= (1 << 24) && ha_.nf2 <= (1 << 24), ErrorCode::Unsupported, "type-3 transform extent too large");
+    const periwave::GaussRule gl = periwave::gauss_legendre(3 * s.w + 20);
+    std::vector<double> amp(gl.nodes.size());
+    for (size_t i = 0; i < amp.size(); ++i) {
+      const double t = 1.0 - gl.nodes[i] * gl.nodes[i];
+      amp[i] = gl.weights[i] * (t <= 0.0 ? 0.0 : std::exp(s.beta * (std::sqrt(t) - 1.0)));
+    }
+    ha_.ngl = static_cast<int>(amp.size());
+    upload(ha_.gl_amp, amp);
+    upload(ha_.gl_z, gl.nodes);
+    ha_.eps = eps;
+  }
+}
+
+double Plan::inner_eps(const Opts& o) const {  // apply.cpp:213
+  return o.nufft_eps > 0.0 ? o.nufft_eps : std::max(1e-14, 0.01 * pz_.eps);
+}
+
+void Plan::ensure_vert_accel(double eps) {
+  const Family& f = *fams_[0];
+  if (!va_.ready) {
+    const periwave::UnitCell& c = pz_.cell;
+    const double kx = c.d / (2.0 * periwave::kPi);
+    long mmax = 0;  // apply.cpp:206-210
+    for (double ph : f.host_phase) mmax = std::max(mmax, std::lround(std::abs(ph) * kx));
+    va_.mmax = static_cast<int>(mmax);
+    va_.nmodes = static_cast<int>(2 * mmax + 1);
+    va_.mg = periwave::interp_nodes_for(pz_.eps);
+    require(va_.mg <= 64, ErrorCode::Unsupported, "at most 64 interpolation lines");
+    const periwave::BarycentricGrid g = periwave::make_barycentric_grid(-0.5 * c.eta, 0.5 * c.eta, va_.mg);
+    va_.lo = g.lo;
+    va_.hi = g.hi;
+    va_.nodes_host = g.nodes;
+    for (int k = 0; k < va_.mg; ++k) {  // quadrature.cpp:291-299 reference coordinates
+      va_.tk[k] = (2.0 * g.nodes[k] - g.lo - g.hi) / (g.hi - g.lo);
+      va_.bw[k] = g.bary_w[k];
+    }
+    upload(va_.nodes, g.nodes);
+    std::vector<std::vector<int>> buckets(va_.nmodes);
+    for (size_t r = 0; r < f.host_phase.size(); ++r)
+      buckets[static_cast<size_t>(std::lround(f.host_phase[r] * kx) + mmax)].push_back(static_cast<int>(r));
+    std::vector<int> start(1, 0), list;
+    for (const auto& b : buckets) {
+      list.insert(list.end(), b.begin(), b.end());
+      start.push_back(static_cast<int>(list.size()));
+    }
+    upload(va_.bucket_start, start);
+    upload(va_.bucket, list);
+    va_.ready = true;
+  }
+  if (va_.eps != eps) {
+    const EsSpec s = es_spec(eps);
+    va_.w = s.w;
+    va_.beta = s.beta;
+    va_.nf = static_cast<int>(grid_size_for_modes(static_cast<size_t>(va_.nmodes), s));
+    upload(va_.fac, deconv_factors(s, static_cast<size_t>(va_.nf), static_cast<size_t>(va_.nmodes)));
+    va_.eps = eps;
+  }
+}
+
+size_t Plan::coeff_size(const Opts& o, periwave::ApplyPath path) {
   size_t n = 0;
   for (const auto& f : fams_) {
     if (f->pressure && !o.with_pressure) continue;
-    n += static_cast<size_t>(f->count) * weight_count(f->ws) * 2;
+    if (vert_accel(*f, o, path)) {
+      ensure_vert_accel(inner_eps(o));
+      n += static_cast<size_t>(va_.mg) * va_.nmodes * 2;  // F lines (type-1 output per Legendre line)
+    } else if (horiz_accel(*f, o, path)) {
+      ensure_horiz_accel(inner_eps(o));
+      n += static_cast<size_t>(ha_.mg) * f->count * 2;  // F_k[r] (type-3 output per line and mode)
+    } else {
+      n += static_cast<size_t>(f->count) * weight_count(f->ws) * 2;
+    }
   }
   return n + kMoments + 3;  // moments, padded to a multiple of 8 bytes * 8
 }
@@ -399,15 +541,82 @@ void Plan::validate(const DevSys& s, const Opts& o, bool far_checks, bool neutra
     require(std::abs(h[2]) <= 1e-12 * h[3], ErrorCode::NotNeutral, "this periodizer requires charges summing to zero");
 }
 
-void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff) {
+SpreadArgs Plan::vert_spread_args(const DevSys& s, bool sources) const {
+  SpreadArgs a;
+  a.pos = PosKind::WrappedX;  // x~ = -wrap(x) 2 pi / d (apply.cpp:219, :247)
+  a.pts = sources ? s.src : s.tgt;
+  a.n = sources ? s.ns : s.nt;
+  a.d = pz_.cell.d;
+  a.kx = 2.0 * periwave::kPi / pz_.cell.d;
+  a.nf = va_.nf;
+  a.h = 2.0 * periwave::kPi / static_cast<double>(va_.nf);
+  a.w = va_.w;
+  a.beta = va_.beta;
+  a.lines = va_.mg;
+  a.bary.lo = va_.lo;
+  a.bary.hi = va_.hi;
+  a.bary.m = va_.mg;
+  for (int k = 0; k < va_.mg; ++k) {
+    a.bary.tk[k] = va_.tk[k];
+    a.bary.bw[k] = va_.bw[k];
+  }
+  a.bary_axis = 0;  // Legendre lines in y
+  return a;
+}
+
+void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path) {
   cudaStream_t st = stream_for(o);
   size_t off = 0;
   for (const auto& fp : fams_) {
     Family& f = *fp;
     if (f.pressure && !o.with_pressure) continue;
     const int k = weight_count(f.ws);
-    const size_t len = static_cast<size_t>(f.count) * k * 2;
     f.raw_offset = off;
+    if (vert_accel(f, o, path)) {
+      // apply.cpp:216-228: c_jk = gamma_k(y_j) q_j spread on each Legendre line, type 1 per line
+      ensure_vert_accel(inner_eps(o));
+      SpreadArgs a = vert_spread_args(s, true);
+      a.c = f.ws == WeightSet::Coef ? reinterpret_cast<const double*>(s.coef) : s.q;
+      a.cplx = f.ws == WeightSet::Coef ? 1 : 0;
+      double* grid = nu_grid_.as<double>(static_cast<size_t>(va_.mg) * va_.nf * 2);
+      launch_spread(a, grid, nu_partial_, sms_, st);
+      fft_lines(grid, va_.nf, va_.mg, +1, st);
+      launch_deconv(grid, va_.mg, va_.nf, va_.nmodes, static_cast<const double*>(va_.fac.get()), coeff + off, st);
+      off += static_cast<size_t>(va_.mg) * va_.nmodes * 2;
+      continue;
+    }
+    if (horiz_accel(f, o, path)) {
+      // apply.cpp:313-319: F_k[r] = sum_j gamma_k(x_j) q_j e^{-i lambda_r y_j} (type 3 per line);
+      // the spread depends on neither the part nor the mode, so it is done once for all lines
+      ensure_horiz_accel(inner_eps(o));
+      SpreadArgs a;
+      a.pos = PosKind::PointY;
+      a.pts = s.src;
+      a.n = s.ns;
+      a.c = f.ws == WeightSet::Coef ? reinterpret_cast<const double*>(s.coef) : s.q;
+      a.cplx = f.ws == WeightSet::Coef ? 1 : 0;
+      a.open = 1;
+      a.inv_h = 1.0 / ha_.hx1;
+      a.nf = ha_.nf1;
+      a.w = ha_.w;
+      a.beta = ha_.beta;
+      a.lines = ha_.mg;
+      a.bary.lo = ha_.lo;
+      a.bary.hi = ha_.hi;
+      a.bary.m = ha_.mg;
+      for (int k = 0; k < ha_.mg; ++k) {
+        a.bary.tk[k] = ha_.tk[k];
+        a.bary.bw[k] = ha_.bw[k];
+      }
+      a.bary_axis = 1;  // Legendre lines in x
+      double* grid = nu_grid_.as<double>(static_cast<size_t>(ha_.mg) * ha_.nf1 * 2);
+      launch_spread(a, grid, nu_partial_, sms_, st);
+      launch_exact_lines(grid, ha_.mg, ha_.nf1, static_cast<const double*>(ha_.neg_lam.get()), f.count, ha_.hx1,
+                         static_cast<const double*>(ha_.fac1.get()), coeff + off, st);
+      off += static_cast<size_t>(ha_.mg) * f.count * 2;
+      continue;
+    }
+    const size_t len = static_cast<size_t>(f.count) * k * 2;
     if (f.count > 0) {
       const int chunks = s.ns == 0 ? 1 : s2pw_chunks(s.ns, f.count, k);
       S2pwArgs a;
@@ -439,9 +648,11 @@ void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff) {
   cuda_check(cudaGetLastError(), "source pass launch");
 }
 
-void Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out) {
+bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out,
+                       periwave::ApplyPath path) {
   cudaStream_t st = stream_for(o);
   const Kind kind = kind_of(pz_);
+  bool accelerated = false;
   // zero the outputs this kind produces, then every family accumulates
   if (s.nt > 0) {
     if (kind == Kind::Scalar) cuda_check(cudaMemsetAsync(out.scalar, 0, s.nt * sizeof(double), st), "memset");
@@ -452,12 +663,64 @@ void Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
     if (o.with_gradient) cuda_check(cudaMemsetAsync(out.gradient, 0, 2 * s.nt * sizeof(double), st), "memset");
   }
   size_t off = 0;
-  const size_t mom_off = coeff_size(o) - kMoments - 3;
+  const size_t mom_off = coeff_size(o, path) - kMoments - 3;
   for (const auto& fp : fams_) {
     Family& f = *fp;
     if (f.pressure && !o.with_pressure) continue;
     const int k = weight_count(f.ws);
-    const size_t len = static_cast<size_t>(f.count) * k * 2;
+    const bool haccel = horiz_accel(f, o, path);
+    if (haccel) {
+      // apply.cpp:321-346 per part: mixing, type 3 lambda -> y per line, barycentric sum in x
+      ensure_horiz_accel(inner_eps(o));
+      const int nr_all = f.count;
+      for (size_t p = 0; p + 1 < ha_.part_start.size() && s.nt > 0; ++p) {
+        const int r0 = ha_.part_start[p], nr = ha_.part_start[p + 1] - r0;
+        if (nr == 0) continue;
+        HmixArgs ma;
+        ma.nr = nr;
+        ma.lines = ha_.mg;
+        ma.stride = nr_all;
+        ma.f_off = r0;
+        ma.decay_s = static_cast<const double*>(f.decay_s.get()) + r0;
+        ma.shift_s = static_cast<const double*>(f.shift_s.get()) + r0;
+        ma.decay_t = static_cast<const double*>(f.decay_t.get()) + r0;
+        ma.shift_t = static_cast<const double*>(f.shift_t.get()) + r0;
+        ma.diag = static_cast<const double*>(f.t[0].get()) + 2 * r0;
+        ma.nodes = static_cast<const double*>(ha_.nodes.get());
+        ma.lam = static_cast<const double*>(f.phase.get()) + r0;
+        ma.inv_h = 1.0 / ha_.hx2;
+        ma.nf = ha_.nf2;
+        ma.w = ha_.w;
+        ma.beta = ha_.beta;
+        double* Aw = nu_lines_.as<double>(static_cast<size_t>(ha_.mg) * nr * 2);
+        launch_hmix(ma, coeff + off, Aw, st);
+        double* grid = nu_grid_.as<double>(static_cast<size_t>(ha_.mg) * ha_.nf2 * 2);
+        launch_lam_spread(ma, Aw, grid, st);
+        HtgtArgs ta2;
+        ta2.nt = s.nt;
+        ta2.tgt = s.tgt;
+        ta2.lo = ha_.lo;
+        ta2.hi = ha_.hi;
+        ta2.lines = ha_.mg;
+        for (int kk = 0; kk < ha_.mg; ++kk) {
+          ta2.tk[kk] = ha_.tk[kk];
+          ta2.bw[kk] = ha_.bw[kk];
+        }
+        ta2.hx = ha_.hx2;
+        ta2.nf = ha_.nf2;
+        ta2.w = ha_.w;
+        ta2.ngl = ha_.ngl;
+        ta2.gl_amp = static_cast<const double*>(ha_.gl_amp.get());
+        ta2.gl_z = static_cast<const double*>(ha_.gl_z.get());
+        launch_htarget(ta2, grid, kind == Kind::Multipole ? nullptr : out.scalar,
+                       kind == Kind::Multipole ? out.complex_scalar : nullptr, st);
+      }
+      accelerated = true;
+      off += static_cast<size_t>(ha_.mg) * f.count * 2;
+      continue;
+    }
+    const bool accel = vert_accel(f, o, path);
+    const size_t len = accel ? static_cast<size_t>(va_.mg) * va_.nmodes * 2 : static_cast<size_t>(f.count) * k * 2;
     double* A = A_.as<double>(static_cast<size_t>(std::max(f.count, 1)) * f.ko * 2);
     double* B = B_.as<double>(static_cast<size_t>(std::max(f.count, 1)) * f.ko * 2);
     double* m0 = m0_.as<double>(8);
@@ -480,7 +743,7 @@ void Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
     pa.three_term = static_cast<const int*>(f.three_term.get());
     pa.A = A;
     pa.B = B;
-    launch_prep(pa, st);
+    if (!accel) launch_prep(pa, st);
     if (f.has_lin || f.has_cst) {
       const double* mv = f.has_lin ? f.mlin : nullptr;
       if (f.has_lin)
@@ -510,10 +773,40 @@ void Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
       ta.out_re = out.scalar;
       ta.out_grad = out.gradient;
     }
-    launch_pw2t(ta, st);
+    if (accel) {
+      // rank-one m0 terms stay direct (apply.cpp:462); no plane-wave modes in this launch
+      ta.modes.count = 0;
+      if (f.has_lin) launch_pw2t(ta, st);
+      if (s.nt > 0) {
+        // apply.cpp:230-258: mode mixing, one type 2 per line, barycentric sum over lines
+        MixArgs ma;
+        ma.nmodes = va_.nmodes;
+        ma.lines = va_.mg;
+        ma.bucket_start = static_cast<const int*>(va_.bucket_start.get());
+        ma.bucket = static_cast<const int*>(va_.bucket.get());
+        ma.decay_s = static_cast<const double*>(f.decay_s.get());
+        ma.shift_s = static_cast<const double*>(f.shift_s.get());
+        ma.decay_t = static_cast<const double*>(f.decay_t.get());
+        ma.shift_t = static_cast<const double*>(f.shift_t.get());
+        ma.diag = static_cast<const double*>(f.t[0].get());
+        ma.nodes = static_cast<const double*>(va_.nodes.get());
+        double* G = nu_lines_.as<double>(static_cast<size_t>(va_.mg) * va_.nmodes * 2);
+        launch_mix(ma, coeff + off, G, st);
+        double* grid = nu_grid_.as<double>(static_cast<size_t>(va_.mg) * va_.nf * 2);
+        launch_precorrect(G, va_.mg, va_.nf, va_.nmodes, static_cast<const double*>(va_.fac.get()), grid, st);
+        fft_lines(grid, va_.nf, va_.mg, -1, st);
+        const SpreadArgs a = vert_spread_args(s, false);
+        launch_interp(a, grid, kind == Kind::Multipole ? nullptr : out.scalar,
+                      kind == Kind::Multipole ? out.complex_scalar : nullptr, true, st);
+      }
+      accelerated = true;
+    } else {
+      launch_pw2t(ta, st);
+    }
     off += len;
   }
   cuda_check(cudaGetLastError(), "target pass launch");
+  return accelerated;
 }
 
 void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
@@ -627,10 +920,11 @@ bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bo
   far_timed_ = near_timed_ = false;
   if (far) {
     validate(s, o, true);
-    double* coeff = coeff_ws_.as<double>(coeff_size(o));
+    const periwave::ApplyPath path = resolve(o, s.ns, s.nt);
+    double* coeff = coeff_ws_.as<double>(coeff_size(o, path));
     cuda_check(cudaEventRecord(ev_[0], st), "event");
-    source_pass(s, o, coeff);
-    target_pass(s, o, coeff, out);
+    source_pass(s, o, coeff, path);
+    accelerated = target_pass(s, o, coeff, out, path);
     cuda_check(cudaEventRecord(ev_[1], st), "event");
     far_timed_ = true;
   }

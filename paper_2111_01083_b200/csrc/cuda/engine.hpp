@@ -91,7 +91,46 @@ struct Family {
   double mlin[4] = {0, 0, 0, 0};
   double mcst[2] = {0, 0};
   size_t raw_offset = 0;  // in the coefficient buffer (doubles)
+  int axis_group = 0;     // scalar families: 0 vertical parts, 1 horizontal parts
+  std::vector<double> host_phase;
+  std::vector<int> part_sizes;  // modes per part, in part order
   ModeTable table() const;
+};
+
+// Accelerated vertical route (apply.cpp:200-259): Legendre lines in y, one type-1
+// transform per line on the sources, mode mixing, one type-2 per line on the targets.
+struct VertAccel {
+  bool ready = false;
+  int mmax = 0, nmodes = 0, mg = 0;
+  double lo = 0.0, hi = 0.0;
+  std::vector<double> nodes_host;
+  DevBuf nodes, bucket_start, bucket;
+  // per inner eps
+  double eps = -1.0;
+  int nf = 0, w = 0;
+  double beta = 0.0;
+  DevBuf fac;
+  // BaryGrid is filled at build time (device copies live in the kernel parameters)
+  double tk[64] = {}, bw[64] = {};
+};
+
+// Accelerated horizontal route of singly periodic cells (apply.cpp:261-348): Legendre
+// lines in x, per part one type-3 transform per line on the sources (y -> -lambda)
+// and one on the targets (lambda -> y). The interval and the y extents are the
+// closed cell's (data-independent, so every rank of a sharded apply builds the
+// same grids).
+struct HorizAccel {
+  bool ready = false;
+  int mg = 0;
+  double lo = 0.0, hi = 0.0, ymax = 0.0, lmax = 0.0;
+  double tk[64] = {}, bw[64] = {};
+  DevBuf nodes, neg_lam;
+  std::vector<int> part_start;  // mode ranges of the parts inside the horizontal family
+  // per inner eps
+  double eps = -1.0;
+  int w = 0, nf1 = 0, nf2 = 0, ngl = 0;
+  double beta = 0.0, hx1 = 0.0, hx2 = 0.0;
+  DevBuf fac1, gl_amp, gl_z;
 };
 
 class Plan {
@@ -106,9 +145,12 @@ class Plan {
 
   // apply_far's checks (apply.cpp:417-422, :350-393) on a device-resident system
   void validate(const DevSys& s, const Opts& o, bool far_checks, bool neutrality = true);
-  size_t coeff_size(const Opts& o) const;
-  void source_pass(const DevSys& s, const Opts& o, double* coeff);
-  void target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out);
+  // the path Auto resolves to for the whole (possibly sharded) problem (apply.cpp:424)
+  periwave::ApplyPath resolve(const Opts& o, size_t n_src_total, size_t n_tgt_total) const;
+  size_t coeff_size(const Opts& o, periwave::ApplyPath path);
+  void source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path);
+  // returns the accelerated flag (apply.cpp:464-471)
+  bool target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out, periwave::ApplyPath path);
   // adds every near image (fused) or one image (single shift)
   void near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy, bool identity);
   // full pipeline on device pointers; returns the accelerated flag
@@ -136,8 +178,20 @@ class Plan {
   cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
   bool far_timed_ = false, near_timed_ = false;
 
+  VertAccel va_;
+  HorizAccel ha_;
+  DevBuf nu_grid_, nu_partial_, nu_lines_;
+  bool horiz_accel(const Family& f, const Opts& o, periwave::ApplyPath path) const;
+  void ensure_horiz_accel(double inner_eps);
+  size_t horiz_coeff_len() const;
+
   void build_families();
   int s2pw_chunks(size_t ns, int modes, int k) const;
+  // a vertical scalar family that takes the NUFFT route on this path
+  bool vert_accel(const Family& f, const Opts& o, periwave::ApplyPath path) const;
+  void ensure_vert_accel(double inner_eps);
+  double inner_eps(const Opts& o) const;
+  SpreadArgs vert_spread_args(const DevSys& s, bool sources) const;
 };
 
 }  // namespace pwb

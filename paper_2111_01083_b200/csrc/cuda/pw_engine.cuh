@@ -161,4 +161,44 @@ constexpr int kReduceBlocks = 296;
 void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_checks, cudaStream_t st);
 void launch_sum_blocks(const double* block_vals, int blocks, int n, double* out, cudaStream_t st);
 
+// ---------------------------------------------------------------- NUFFT lines (nufft.cu)
+constexpr int kMaxLines = 64;
+
+// Legendre interpolation grid (quadrature.cpp:258-304) in reference coordinates.
+struct BaryGrid {
+  double lo = 0.0, hi = 0.0;
+  int m = 0;  // 0: no barycentric lines (a single line of weight 1)
+  double tk[kMaxLines] = {};
+  double bw[kMaxLines] = {};
+};
+
+enum class PosKind : int { Array = 0, WrappedX = 1, PointY = 2 };
+
+struct SpreadArgs {
+  size_t n = 0;                  // points
+  PosKind pos = PosKind::Array;  // how the spreading coordinate is formed
+  const double* xs = nullptr;    // PosKind::Array
+  const double2* pts = nullptr;  // WrappedX / PointY (also the barycentric coordinate source)
+  double d = 1.0, kx = 1.0;      // WrappedX: -wrap(x, d) * kx
+  const double* c = nullptr;     // strengths (spread only)
+  int cplx = 0;                  // strengths complex interleaved (else real)
+  int open = 0;                  // open grid (type 3): t = p / hx + nf / 2
+  double h = 1.0, inv_h = 1.0;
+  int nf = 0, w = 3;
+  double beta = 6.9;
+  int lines = 1, lpg = 1;
+  BaryGrid bary;                 // line weights from the barycentric row (m > 0)
+  int bary_axis = 0;             // 0: y coordinate, 1: x coordinate of pts
+  size_t per_chunk = 0;
+};
+
+struct MixArgs {
+  int nmodes = 0, lines = 0;
+  const int* bucket_start = nullptr;  // [nmodes + 1]
+  const int* bucket = nullptr;        // mode ids (vertical family indices), part order
+  const double *decay_s = nullptr, *shift_s = nullptr, *decay_t = nullptr, *shift_t = nullptr;
+  const double* diag = nullptr;       // complex per mode
+  const double* nodes = nullptr;      // [lines] interpolation nodes (device)
+};
+
 }  // namespace pwb
