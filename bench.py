@@ -243,8 +243,9 @@ def main():
     cell = pw.make_unit_cell(c.cell[0], c.cell[1], c.cell[2], c.cell[3])
     pz = pw.make_periodizer(c.pde, c.beta, cell, c.eps)
     ns, nt = len(inp.sources), len(inp.targets)
-    t_lo, t_hi = (nt * rank) // ws, (nt * (rank + 1)) // ws
-    s_lo, s_hi = (ns * rank) // ws, (ns * (rank + 1)) // ws
+    from paper_2111_01083_b200.dist import target_slice
+
+    t_lo, t_hi = target_slice(nt, ws, rank)  # rank's targets (outputs stay sharded)
     kw_name = "charges" if c.strength == "charge" else "forces"
     strength = inp.charges if c.strength == "charge" else inp.forces
 
@@ -257,20 +258,23 @@ def main():
     opt = pw.ApplyOptions(path=pw.ApplyPath.Auto, with_gradient=c.gradient, stream=stream.cuda_stream)
     full = pw.ParticleSystem(sources=src_d, targets=tgt_d, **{kw_name: str_d})
     out = pw.FieldResult()
-    coeff = None
+    from paper_2111_01083_b200 import dist as pdist
+
+    symmetric = not c.separate_targets
     if ws > 1:
-        coeff = torch.zeros(pw.far_coeff_size(pz, opt), dtype=torch.float64, device=dev)
-        src_shard = pw.ParticleSystem(sources=src_d[s_lo:s_hi], **{kw_name: str_d[s_lo:s_hi]})
+        tgt_all = None if symmetric else torch.from_numpy(np.ascontiguousarray(inp.targets)).to(dev)
+        backend = pdist.CudaBackend(pw, pz, opt, src_d, str_d, kw_name, tgt_all)
+        plan = pdist.ShardPlan(ns, nt, ws, rank)
+        comm = pdist.Comm(ws)
 
     def step():
         nonlocal out
         if ws == 1:
             out = pw.total_field(pz, full, opt)
             return
-        pw.far_source_pass(pz, src_shard, coeff, opt)
-        dist.all_reduce(coeff)  # one ncclAllReduce(fp64, sum) of the plane-wave coefficients
-        out = pw.far_target_pass(pz, full, coeff, opt, out)
-        pw.near_field(pz, full, opt, out)
+        # S2PW on my source slice + allreduce(fp64) of the coefficients; PW2T on my target
+        # slice; symmetric near items + reduce-scatter(int64) of the fixed-point sums
+        out, _ = pdist.sharded_total_field(backend, comm, plan, symmetric)
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # > 126 MB L2
     for _ in range(args.warmup):
@@ -311,6 +315,7 @@ def main():
     src_h = torch.from_numpy(inp.sources).pin_memory()
     str_h = torch.from_numpy(strength).pin_memory()
     tgt_h = src_h if same else torch.from_numpy(np.ascontiguousarray(inp.targets[t_lo:t_hi])).pin_memory()
+    tgt_all_h = None if not c.separate_targets else torch.from_numpy(np.ascontiguousarray(inp.targets)).pin_memory()
     e2e_ms = []
     host_sys = pw.ParticleSystem(sources=src_h, targets=tgt_h, **{kw_name: str_h})
     for k in range(args.e2e_steps + 1):
@@ -324,13 +329,9 @@ def main():
         else:
             s_d = src_h.to(dev, non_blocking=True)
             q_d = str_h.to(dev, non_blocking=True)
-            t_d = tgt_h.to(dev, non_blocking=True)
-            fs = pw.ParticleSystem(sources=s_d, targets=t_d, **{kw_name: q_d})
-            sh = pw.ParticleSystem(sources=s_d[s_lo:s_hi], **{kw_name: q_d[s_lo:s_hi]})
-            pw.far_source_pass(pz, sh, coeff, opt)
-            dist.all_reduce(coeff)
-            rr = pw.far_target_pass(pz, fs, coeff, opt)
-            pw.near_field(pz, fs, opt, rr)
+            t_d = None if symmetric else tgt_all_h.to(dev, non_blocking=True)
+            be = pdist.CudaBackend(pw, pz, opt, s_d, q_d, kw_name, t_d)
+            rr, _ = pdist.sharded_total_field(be, comm, plan, symmetric)
             host_out = (rr.scalar if rr.scalar is not None else rr.velocity).to("cpu", non_blocking=True)
         e1.record(stream)
         e1.synchronize()
@@ -342,7 +343,8 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt[0])
     nout = 1 if c.strength == "charge" else 2
-    h2d = 8 * (2 * ns + (1 if c.strength == "charge" else 2) * ns + (0 if same else 2 * (t_hi - t_lo)))
+    # bytes of the tensors copied per e2e step: sources + strengths (+ targets when separate)
+    h2d = 8 * (2 * ns + (1 if c.strength == "charge" else 2) * ns) + (16 * nt if c.separate_targets else 0)
     d2h = 8 * nout * (t_hi - t_lo) + (16 * (t_hi - t_lo) if c.gradient else 0)
 
     # ---- roofline of the dominant kernel (fused near-image P2P tile)
@@ -351,7 +353,8 @@ def main():
     peak = ctypes.c_double(0.0)
     pw.lib().pwb_fp64_peak_probe(-1, ctypes.byref(peak))
     nimg = len(pw.near_translations(cell))
-    pairs = nimg * ns * (t_hi - t_lo)
+    # pairs handled by this rank's near launch (symmetric items split evenly across ranks)
+    pairs = nimg * ns * nt / ws if (symmetric and ws > 1) else nimg * ns * (t_hi - t_lo)
     flops_near = pairs * F_PAIR[args.config]
     achieved = flops_near / (t_near * 1e-3) / 1e12
     rank_far = pz.rank()

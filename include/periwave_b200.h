@@ -199,6 +199,18 @@ int pwb_far_source_pass(const pwb_periodizer* pz, const pwb_system* sys, const p
                         size_t n_src_total, size_t n_tgt_total, double* coeff_dev);
 int pwb_far_target_pass(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt,
                         size_t n_src_total, size_t n_tgt_total, const double* coeff_dev, pwb_field* out);
+/* Sharded symmetric near field (targets == sources). The unordered pairs are cut
+ * into `*n_items` work items (host-only query); each rank runs a disjoint item
+ * range into its own fixed-point accumulator acc (device, zeroed by the caller,
+ * n * nout * 3 int64, target-major: acc[(l*nout + c)*3 + limb]); the accumulators
+ * are summed exactly as integers (e.g. ncclReduceScatter(ncclInt64, sum) so each
+ * rank receives a contiguous slice of targets), and pwb_fixed_to_field adds a
+ * slice into the outputs. Bitwise deterministic for any split. */
+int pwb_near_sym_items(const pwb_periodizer* pz, size_t n, const pwb_options* opt, long* n_items, int* nout);
+int pwb_near_sym_partial(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, long item_begin,
+                         long item_end, int64_t* acc);
+int pwb_fixed_to_field(const pwb_periodizer* pz, const pwb_options* opt, const int64_t* acc, size_t n_targets,
+                       pwb_field* out);
 /* Strength/neutrality/cell checks of apply_far (proj/src/apply.cpp:350-393, cell.cpp:77-94),
  * evaluated on the device for device-resident systems. */
 int pwb_validate(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt);

@@ -133,6 +133,7 @@ EXPORTED = [
     "pwb_far_coeff_size", "pwb_far_source_pass", "pwb_far_target_pass", "pwb_validate",
     "pwb_nufft_type1", "pwb_nufft_type2", "pwb_nufft_type3", "pwb_fast_nufft_available",
     "pwb_eval_kernel", "pwb_rng_uniform", "pwb_launch_count", "pwb_last_phase_ms", "pwb_fp64_peak_probe",
+    "pwb_near_sym_items", "pwb_near_sym_partial", "pwb_fixed_to_field",
 ]
 
 _lib = None
@@ -184,6 +185,11 @@ def lib() -> ctypes.CDLL:
     L.pwb_launch_count.argtypes = [ctypes.POINTER(ctypes.c_long)]
     L.pwb_last_phase_ms.argtypes = [vp, i, ctypes.POINTER(d), ctypes.POINTER(d)]
     L.pwb_fp64_peak_probe.argtypes = [i, ctypes.POINTER(d)]
+    L.pwb_near_sym_items.argtypes = [vp, sz, ctypes.POINTER(_Options), ctypes.POINTER(ctypes.c_long),
+                                     ctypes.POINTER(i)]
+    L.pwb_near_sym_partial.argtypes = [vp, ctypes.POINTER(_System), ctypes.POINTER(_Options), ctypes.c_long,
+                                       ctypes.c_long, vp]
+    L.pwb_fixed_to_field.argtypes = [vp, ctypes.POINTER(_Options), vp, sz, ctypes.POINTER(_Field)]
     _lib = L
     return L
 
@@ -544,10 +550,9 @@ def fast_nufft_available() -> bool:
 
 
 def _cplx(a) -> np.ndarray:
+    """Any 1-D real/complex array -> interleaved (re, im) float64 of shape (n, 2)."""
     a = np.asarray(a)
-    if np.iscomplexobj(a):
-        return np.ascontiguousarray(np.stack([a.real, a.imag], axis=-1), dtype=np.float64)
-    return np.ascontiguousarray(a, dtype=np.float64)
+    return np.ascontiguousarray(np.stack([a.real, a.imag], axis=-1), dtype=np.float64)
 
 
 def nufft_type1(backend: NufftBackend, eps: float, x, c, nmodes: int) -> np.ndarray:
@@ -590,31 +595,67 @@ def eval_kernel(which: int, pde: int, beta: float, l: int, inputs: np.ndarray) -
 
 
 # ---------------------------------------------------------------- sharded far field (multi-GPU)
-def far_coeff_size(pz: Periodizer, opt: Optional[ApplyOptions] = None) -> int:
+def far_coeff_size(pz: Periodizer, opt: Optional[ApplyOptions] = None, n_src_total: int = 0,
+                   n_tgt_total: int = 0) -> int:
+    """Doubles in the plane-wave coefficient buffer (the allreduce operand); the path is
+    resolved from the global counts (0: the local system is the whole problem)."""
     n = ctypes.c_size_t(0)
     o = (opt or ApplyOptions())._c()
-    _check(lib().pwb_far_coeff_size(pz.handle, ctypes.byref(o), 0, 0, ctypes.byref(n)))
+    _check(lib().pwb_far_coeff_size(pz.handle, ctypes.byref(o), n_src_total, n_tgt_total, ctypes.byref(n)))
     return n.value
 
 
-def far_source_pass(pz: Periodizer, sys: ParticleSystem, coeff, opt: Optional[ApplyOptions] = None) -> None:
+def far_source_pass(pz: Periodizer, sys: ParticleSystem, coeff, opt: Optional[ApplyOptions] = None,
+                    n_src_total: int = 0, n_tgt_total: int = 0) -> None:
     s, mem = sys._c()
     if mem != MEM_DEVICE:
         raise ValueError("far_source_pass takes device tensors")
     o = (opt or ApplyOptions())._c()
-    _check(lib().pwb_far_source_pass(pz.handle, ctypes.byref(s), ctypes.byref(o), 0, 0, coeff.data_ptr()))
+    _check(lib().pwb_far_source_pass(pz.handle, ctypes.byref(s), ctypes.byref(o), n_src_total, n_tgt_total,
+                                     coeff.data_ptr()))
 
 
 def far_target_pass(pz: Periodizer, sys: ParticleSystem, coeff, opt: Optional[ApplyOptions] = None,
-                    out: Optional[FieldResult] = None) -> FieldResult:
+                    out: Optional[FieldResult] = None, n_src_total: int = 0, n_tgt_total: int = 0) -> FieldResult:
     opt = opt or ApplyOptions()
     s, mem = sys._c()
     if mem != MEM_DEVICE:
         raise ValueError("far_target_pass takes device tensors")
     res, f = _field_for(pz, opt, s.n_tgt, True, sys.targets, out)
     o = opt._c()
-    _check(lib().pwb_far_target_pass(pz.handle, ctypes.byref(s), ctypes.byref(o), 0, 0, coeff.data_ptr(),
-                                     ctypes.byref(f)))
+    _check(lib().pwb_far_target_pass(pz.handle, ctypes.byref(s), ctypes.byref(o), n_src_total, n_tgt_total,
+                                     coeff.data_ptr(), ctypes.byref(f)))
+    res.accelerated = bool(f.accelerated)
+    return res
+
+
+def near_sym_items(pz: Periodizer, n: int, opt: Optional[ApplyOptions] = None):
+    """(work items, outputs per target) of the symmetric near decomposition (host only)."""
+    items, nout = ctypes.c_long(0), ctypes.c_int(0)
+    o = (opt or ApplyOptions())._c()
+    _check(lib().pwb_near_sym_items(pz.handle, n, ctypes.byref(o), ctypes.byref(items), ctypes.byref(nout)))
+    return items.value, nout.value
+
+
+def near_sym_partial(pz: Periodizer, sys: ParticleSystem, acc, item_begin: int, item_end: int,
+                     opt: Optional[ApplyOptions] = None) -> None:
+    """Adds work items [begin, end) of the symmetric near field into the int64 accumulator
+    `acc` (device, n * nout * 3, target-major). sys.targets must be sys.sources."""
+    s, mem = sys._c()
+    if mem != MEM_DEVICE:
+        raise ValueError("near_sym_partial takes device tensors")
+    o = (opt or ApplyOptions())._c()
+    _check(lib().pwb_near_sym_partial(pz.handle, ctypes.byref(s), ctypes.byref(o), item_begin, item_end,
+                                      acc.data_ptr()))
+
+
+def fixed_to_field(pz: Periodizer, acc, n_targets: int, out: FieldResult, opt: Optional[ApplyOptions] = None,
+                   like=None) -> FieldResult:
+    """out += the fp64 value of a fixed-point accumulator slice (device)."""
+    opt = opt or ApplyOptions()
+    res, f = _field_for(pz, opt, n_targets, True, like if like is not None else acc, out)
+    o = opt._c()
+    _check(lib().pwb_fixed_to_field(pz.handle, ctypes.byref(o), acc.data_ptr(), n_targets, ctypes.byref(f)))
     return res
 
 

@@ -654,6 +654,49 @@ int pwb_far_target_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_
   });
 }
 
+int pwb_near_sym_items(const pwb_periodizer* h, size_t n, const pwb_options* o, long* n_items, int* nout) {
+  if (!h || !n_items) return fail_arg("null argument");
+  return guard([&] {
+    const pwb::Opts opt = opts_from(o);
+    const pwb::NearKind k = pwb::near_kind_of(h->pz, opt.with_pressure, opt.with_gradient);
+    *n_items = pwb::near_sym_item_count(k, n);
+    if (nout) *nout = static_cast<int>(pwb::near_outputs(k));
+    return OK;
+  });
+}
+
+int pwb_near_sym_partial(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, long item_begin,
+                         long item_end, int64_t* acc) {
+  if (!h || !s || !acc) return fail_arg("null argument");
+  if (s->memory != PWB_MEM_DEVICE) return fail_arg("sharded passes take device memory");
+  return guard([&] {
+    const int dev = current_device(o ? o->device : -1);
+    pwb::Plan& p = const_cast<pwb_periodizer*>(h)->plan(dev);
+    std::lock_guard<std::mutex> lock(p.mutex());
+    pwb::Opts opt = opts_from(o);
+    pwb::DevSys ds;
+    stage_in(p, s, p.stream_for(opt), &ds);
+    p.validate(ds, opt, false, /*neutrality=*/true);
+    p.sym_partial(ds, opt, item_begin, item_end, reinterpret_cast<unsigned long long*>(acc));
+    return OK;
+  });
+}
+
+int pwb_fixed_to_field(const pwb_periodizer* h, const pwb_options* o, const int64_t* acc, size_t n, pwb_field* f) {
+  if (!h || !acc || !f) return fail_arg("null argument");
+  if (f->memory != PWB_MEM_DEVICE) return fail_arg("fixed-point conversion takes device memory");
+  return guard([&] {
+    const int dev = current_device(o ? o->device : -1);
+    pwb::Plan& p = const_cast<pwb_periodizer*>(h)->plan(dev);
+    std::lock_guard<std::mutex> lock(p.mutex());
+    pwb::Opts opt = opts_from(o);
+    pwb::DevOut dout;
+    stage_out(p, f, n, p.stream_for(opt), false, &dout);
+    p.fixed_finish(opt, reinterpret_cast<const unsigned long long*>(acc), n, dout);
+    return OK;
+  });
+}
+
 int pwb_validate(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o) {
   if (!h || !s) return fail_arg("null argument");
   return guard([&] {

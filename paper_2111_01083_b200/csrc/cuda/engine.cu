@@ -67,6 +67,17 @@ Kind kind_of(const periwave::Periodizer& pz) {  // apply.cpp:20-26
   return Kind::Scalar;
 }
 
+NearKind near_kind_of(const periwave::Periodizer& pz, bool with_pressure, bool with_gradient) {
+  const Kind kind = kind_of(pz);
+  if (kind == Kind::Multipole) return NearKind::Multipole;
+  if (pz.dlp) return NearKind::Stresslet;
+  if (kind == Kind::Velocity)
+    return pz.pde == periwave::Pde::Stokes ? (with_pressure ? NearKind::StokesP : NearKind::Stokes)
+                                           : (with_pressure ? NearKind::ModStokesP : NearKind::ModStokes);
+  if (pz.pde == periwave::Pde::ModHelmholtz) return with_gradient ? NearKind::ModHelmGrad : NearKind::ModHelm;
+  return NearKind::Laplace;
+}
+
 ModeTable Family::table() const {
   ModeTable t;
   t.phase = static_cast<const double*>(phase.get());
@@ -809,13 +820,10 @@ bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
   return accelerated;
 }
 
-void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
-                bool identity) {
-  if (s.nt == 0 || s.ns == 0) return;
-  cudaStream_t st = stream_for(o);
+NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
+                         bool identity, NearArgs& a) const {
   const Kind kind = kind_of(pz_);
   NearKind nk;
-  NearArgs a;
   a.tgt = s.tgt;
   a.nt = s.nt;
   a.src = s.src;
@@ -885,6 +893,65 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
       a.id_img = 1;
     }
   }
+  return nk;
+}
+
+long Plan::sym_items(const Opts& o, size_t n) {
+  DevSys s;
+  s.ns = s.nt = n;
+  NearArgs a;
+  const NearKind nk = near_args(s, o, DevOut{}, false, 0, 0, false, a);
+  if (!near_sym_supported(nk) || n == 0) return 0;
+  return near_sym_item_count(nk, n);
+}
+
+int Plan::near_nout(const Opts& o) const {
+  NearArgs a;
+  return static_cast<int>(near_outputs(near_args(DevSys{}, o, DevOut{}, false, 0, 0, false, a)));
+}
+
+void Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc) {
+  require(s.tgt == s.src && s.nt == s.ns, ErrorCode::Unsupported,
+          "the symmetric near field needs the sources as targets");
+  cudaStream_t st = stream_for(o);
+  NearArgs a;
+  const NearKind nk = near_args(s, o, DevOut{}, false, 0, 0, false, a);
+  require(near_sym_supported(nk), ErrorCode::Unsupported, "no symmetric near tile for this kernel");
+  int* flag = flag_.as<int>(1);
+  cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
+  a.flag = flag;
+  const size_t nb = near_sym_tiles(s.nt);
+  int* rs_dev = sym_rows_.as<int>(nb + 1);
+  int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
+  SymRange r;
+  r.begin = begin;
+  r.end = end;
+  r.finish = false;
+  cuda_check(cudaEventRecord(ev_[2], st), "event");
+  launch_near_sym(nk, a, st, acc, rs_dev, rs_host, r);
+  cuda_check(cudaEventRecord(ev_[3], st), "event");
+  near_timed_ = true;
+  cuda_check(cudaGetLastError(), "near launch");
+  int* hflag = static_cast<int*>(host_checks_.ensure(64 * sizeof(double)));
+  cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+  cuda_check(cudaStreamSynchronize(st), "near sync");
+  require(*hflag == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
+}
+
+void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, const DevOut& out) {
+  NearArgs a;
+  near_args(DevSys{}, o, out, false, 0, 0, false, a);
+  launch_fx_finish(acc, n, a.out0, a.nout0, a.out1, a.nout1, stream_for(o));
+  cuda_check(cudaGetLastError(), "fixed-point finish");
+  cuda_check(cudaStreamSynchronize(stream_for(o)), "sync");
+}
+
+void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
+                bool identity) {
+  if (s.nt == 0 || s.ns == 0) return;
+  cudaStream_t st = stream_for(o);
+  NearArgs a;
+  const NearKind nk = near_args(s, o, out, single, shx, shy, identity, a);
   int* flag = flag_.as<int>(1);
   cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
   a.flag = flag;
@@ -899,7 +966,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
     auto* fx = sym_fx_.as<unsigned long long>(3 * s.nt * nout);
     int* rs_dev = sym_rows_.as<int>(nb + 1);
     int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
-    done = launch_near_sym(nk, a, st, fx, rs_dev, rs_host);
+    done = launch_near_sym(nk, a, st, fx, rs_dev, rs_host, SymRange{});
   }
   if (!done) {
     double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);

@@ -74,6 +74,8 @@ struct Opts {
 
 enum class Kind { Scalar, Velocity, Multipole };
 Kind kind_of(const periwave::Periodizer& pz);
+// which near-field tile the periodizer and options select (host only)
+NearKind near_kind_of(const periwave::Periodizer& pz, bool with_pressure, bool with_gradient);
 
 // One family of plane-wave parts that share a weight set and output shape.
 struct Family {
@@ -153,6 +155,12 @@ class Plan {
   bool target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out, periwave::ApplyPath path);
   // adds every near image (fused) or one image (single shift)
   void near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy, bool identity);
+  // multi-GPU symmetric near field: work items of the triangle decomposition for n
+  // points, a range of them into a fixed-point accumulator, and its conversion
+  long sym_items(const Opts& o, size_t n);
+  int near_nout(const Opts& o) const;
+  void sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc);
+  void fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, const DevOut& out);
   // full pipeline on device pointers; returns the accelerated flag
   bool total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images);
 
@@ -187,6 +195,8 @@ class Plan {
 
   void build_families();
   int s2pw_chunks(size_t ns, int modes, int k) const;
+  NearKind near_args(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
+                     bool identity, NearArgs& a) const;
   // a vertical scalar family that takes the NUFFT route on this path
   bool vert_accel(const Family& f, const Opts& o, periwave::ApplyPath path) const;
   void ensure_vert_accel(double inner_eps);

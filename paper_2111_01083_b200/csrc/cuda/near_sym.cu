@@ -26,6 +26,8 @@
 // is converted back to fp64 once at the end.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "near_common.cuh"
 #include "pw_engine.cuh"
 #include "pw_math.cuh"
@@ -39,16 +41,18 @@ constexpr int kWarps = kT / 32;
 
 // ---------------------------------------------------------------- fixed point
 // v = a 2^22 + b 2^-20 + c 2^-62; limbs truncate toward zero so each carries the
-// sign of v and each remainder is exact.
-__device__ __forceinline__ void fx_add(unsigned long long* base, size_t stride, double v) {
+// sign of v and each remainder is exact. Layout: target-major, the three limbs of
+// output c of target l at acc[(l * nout + c) * 3 + {0,1,2}], so a contiguous slice of
+// targets is a contiguous slice of the buffer (the multi-GPU reduce-scatter operand).
+__device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
   const double a = trunc(v * 0x1p-22);
   const double r1 = fma(-a, 0x1p22, v);
   const double b = trunc(r1 * 0x1p20);
   const double r2 = fma(-b, 0x1p-20, r1);
   const double c = rint(r2 * 0x1p62);
-  atomicAdd(base, static_cast<unsigned long long>(static_cast<long long>(a)));
-  atomicAdd(base + stride, static_cast<unsigned long long>(static_cast<long long>(b)));
-  atomicAdd(base + 2 * stride, static_cast<unsigned long long>(static_cast<long long>(c)));
+  atomicAdd(p, static_cast<unsigned long long>(static_cast<long long>(a)));
+  atomicAdd(p + 1, static_cast<unsigned long long>(static_cast<long long>(b)));
+  atomicAdd(p + 2, static_cast<unsigned long long>(static_cast<long long>(c)));
 }
 
 __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double* out0, int nout0, double* out1,
@@ -56,9 +60,9 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int nout = nout0 + nout1;
   if (i >= n * nout) return;
-  const long long a = static_cast<long long>(acc[i]);
-  const long long b = static_cast<long long>(acc[n * nout + i]);
-  const long long c = static_cast<long long>(acc[2 * n * nout + i]);
+  const long long a = static_cast<long long>(acc[3 * i]);
+  const long long b = static_cast<long long>(acc[3 * i + 1]);
+  const long long c = static_cast<long long>(acc[3 * i + 2]);
   const double v = fma(static_cast<double>(a), 0x1p22,
                        fma(static_cast<double>(b), 0x1p-20, static_cast<double>(c) * 0x1p-62));
   const size_t l = i / nout;
@@ -277,7 +281,8 @@ struct SymArgs {
   int nb;                  // number of TILE-point tiles
   int chunk;               // column tiles per work item
   const int* row_start;    // [nb + 1] first work item of each row tile
-  unsigned long long* fx;  // fixed-point accumulators [3][n][nout]
+  unsigned long long* fx;  // fixed-point accumulators [n][nout][3]
+  int item0;               // first work item of this launch (multi-GPU item ranges)
 };
 
 template <class K>
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
   __shared__ double s_col[kWarps][K::NACC][TILE];
 
   // work item -> (row tile I, first column tile)
-  const int item = blockIdx.x;
+  const int item = S.item0 + static_cast<int>(blockIdx.x);
   int lo = 0, hi = S.nb;  // row_start[I] <= item < row_start[I+1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
       double o[K::NOUT];
       K::finish(acc, a, o);
 #pragma unroll
-      for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + j * K::NOUT + c, n * K::NOUT, o[c]);
+      for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (j * K::NOUT + c) * 3, o[c]);
     }
   }
   if (flag) atomicOr(a.flag, 1);
@@ -458,13 +463,13 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
     double o[K::NOUT];
     K::finish(racc[k], a, o);
 #pragma unroll
-    for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + l * K::NOUT + c, n * K::NOUT, o[c]);
+    for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (l * K::NOUT + c) * 3, o[c]);
   }
 }
 
 template <class K, int NXI, int NROW>
 void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                      int* row_start_host) {
+                      int* row_start_host, const SymRange& range) {
   constexpr int TILE = kT * K::TPT;
   const int chunk = K::CHUNK;
   const int nb = static_cast<int>((a.nt + TILE - 1) / TILE);
@@ -474,51 +479,90 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
     items += (nb - I + chunk - 1) / chunk;
   }
   row_start_host[nb] = items;
+  if (range.total_items) *range.total_items = items;
+  if (range.count_only) return;
+  const long b = range.begin < 0 ? 0 : std::min<long>(range.begin, items);
+  const long e = range.end < 0 ? items : std::min<long>(range.end, items);
   cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
              "row starts");
   const size_t nout = K::NOUT;
-  cuda_check(cudaMemsetAsync(fx, 0, 3 * a.nt * nout * sizeof(unsigned long long), st), "memset fx");
+  if (range.finish) cuda_check(cudaMemsetAsync(fx, 0, 3 * a.nt * nout * sizeof(unsigned long long), st), "memset fx");
   SymArgs S;
   S.a = a;
   S.nb = nb;
   S.chunk = chunk;
   S.row_start = row_start_dev;
   S.fx = fx;
-  near_sym_kernel<K, NXI, NROW><<<items, kT, 0, st>>>(S);
-  const size_t total = a.nt * nout;
-  fx_finish_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(fx, a.nt, a.out0, a.nout0, a.out1,
-                                                                              a.nout1);
-  count_launches(2);
+  S.item0 = static_cast<int>(b);
+  if (e > b) {
+    near_sym_kernel<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
+    count_launches(1);
+  }
+  if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, st);
 }
 
 template <class K>
-bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh) {
-  if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh), true;
-  if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh), true;
-  if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh), true;
-  if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh), true;
+bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
+                  const SymRange& r) {
+  if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh, r), true;
+  if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh, r), true;
+  if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh, r), true;
+  if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh, r), true;
   return false;
 }
 
 }  // namespace
 
+void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int nout0, double* out1, int nout1,
+                      cudaStream_t st) {
+  const size_t total = n * static_cast<size_t>(nout0 + nout1);
+  if (total == 0) return;
+  fx_finish_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(fx, n, out0, nout0, out1, nout1);
+  count_launches(1);
+}
+
 // upper bound on the number of tiles (the smallest tile is 256 points)
 size_t near_sym_tiles(size_t n) { return (n + 255) / 256; }
+
+namespace {
+template <class K>
+long item_count(size_t n) {
+  const size_t tile = static_cast<size_t>(kT) * K::TPT;
+  const long nb = static_cast<long>((n + tile - 1) / tile);
+  long items = 0;
+  for (long I = 0; I < nb; ++I) items += (nb - I + K::CHUNK - 1) / K::CHUNK;
+  return items;
+}
+}  // namespace
+
+long near_sym_item_count(NearKind kind, size_t n) {
+  switch (kind) {
+    case NearKind::Laplace: return item_count<SymLaplace>(n);
+    case NearKind::ModHelm: return item_count<SymModHelm<false>>(n);
+    case NearKind::ModHelmGrad: return item_count<SymModHelm<true>>(n);
+    case NearKind::Stokes: return item_count<SymStokes<false>>(n);
+    case NearKind::StokesP: return item_count<SymStokes<true>>(n);
+    default: return 0;
+  }
+}
 
 bool near_sym_supported(NearKind kind) {
   return kind == NearKind::Laplace || kind == NearKind::ModHelm || kind == NearKind::ModHelmGrad ||
          kind == NearKind::Stokes || kind == NearKind::StokesP;
 }
 
-bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                     int* row_start_host) {
-  if (a.nt == 0) return true;
+bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
+                     const SymRange& r) {
+  if (a.nt == 0) {
+    if (r.total_items) *r.total_items = 0;
+    return true;
+  }
   switch (kind) {
-    case NearKind::Laplace: return dispatch_sym<SymLaplace>(a, st, fx, row_start_dev, row_start_host);
-    case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, row_start_dev, row_start_host);
-    case NearKind::ModHelmGrad: return dispatch_sym<SymModHelm<true>>(a, st, fx, row_start_dev, row_start_host);
-    case NearKind::Stokes: return dispatch_sym<SymStokes<false>>(a, st, fx, row_start_dev, row_start_host);
-    case NearKind::StokesP: return dispatch_sym<SymStokes<true>>(a, st, fx, row_start_dev, row_start_host);
+    case NearKind::Laplace: return dispatch_sym<SymLaplace>(a, st, fx, rsd, rsh, r);
+    case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, rsd, rsh, r);
+    case NearKind::ModHelmGrad: return dispatch_sym<SymModHelm<true>>(a, st, fx, rsd, rsh, r);
+    case NearKind::Stokes: return dispatch_sym<SymStokes<false>>(a, st, fx, rsd, rsh, r);
+    case NearKind::StokesP: return dispatch_sym<SymStokes<true>>(a, st, fx, rsd, rsh, r);
     default: return false;
   }
 }

@@ -59,8 +59,22 @@ void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* part
 // (device and pinned host). Returns false when the kind/layout has no symmetric form.
 bool near_sym_supported(NearKind kind);
 size_t near_sym_tiles(size_t n);
+// Work-item range of one launch: the default is the whole triangle with the
+// accumulator zeroed first and converted into the outputs at the end (finish);
+// multi-GPU ranks run disjoint item ranges into their own accumulator (finish =
+// false), sum the accumulators (integer reduce-scatter) and convert their slice.
+struct SymRange {
+  long begin = -1, end = -1;
+  bool finish = true;
+  bool count_only = false;
+  long* total_items = nullptr;
+};
 bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                     int* row_start_host);
+                     int* row_start_host, const SymRange& range);
+void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int nout0, double* out1, int nout1,
+                      cudaStream_t st);
+// host-only: number of work items of the symmetric decomposition (0 if none)
+long near_sym_item_count(NearKind kind, size_t n);
 
 // ---------------------------------------------------------------- far field (direct S2PW / PW2T)
 // Weight sets: what each source contributes per mode (K real weights).

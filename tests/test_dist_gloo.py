@@ -1,0 +1,249 @@
+"""Multi-rank host logic of the sharded total_field (paper_2111_01083_b200/dist.py) on
+CPU: world_size 2 over gloo, with a NumPy stand-in for the device passes that follows
+the same decomposition (source slices + coefficient all-reduce for the far field;
+triangle work items + int64 fixed-point reduce-scatter for the symmetric near field).
+Checks: every target slice and work item is covered once, the two-rank result equals
+the one-rank result (near part bitwise), and both match the direct sums."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+TILE, CHUNK = 4, 2
+
+
+def _fx_split(v):
+    a = np.trunc(v * 2.0 ** -22)
+    r1 = v - a * 2.0 ** 22
+    b = np.trunc(r1 * 2.0 ** 20)
+    r2 = r1 - b * 2.0 ** -20
+    c = np.rint(r2 * 2.0 ** 62)
+    return np.stack([a, b, c], -1).astype(np.int64)
+
+
+def _fx_value(acc):
+    a, b, c = acc[..., 0].astype(np.float64), acc[..., 1].astype(np.float64), acc[..., 2].astype(np.float64)
+    return a * 2.0 ** 22 + (b * 2.0 ** -20 + c * 2.0 ** -62)
+
+
+class NumpyBackend:
+    """CPU stand-in: direct plane-wave sums over the product's own tables and the
+    image-summed Laplace pair kernel."""
+
+    def __init__(self, pw, pz, src, q):
+        import torch
+
+        self.torch = torch
+        self.src, self.q, self.n = src, q, len(src)
+        self.parts = pz.parts(pw.PART_SCALAR)
+        from oracle.pyoracle import near_shifts
+
+        info = pz.info()
+        c = info["cell"]
+        self.shifts, self.ident = near_shifts((c.d, c.xi, c.eta, int(c.periodicity)))
+        self.nmodes = sum(p.size for p in self.parts)
+
+    def _mode_factors(self, pts, target):
+        out = []
+        for p in self.parts:
+            w = pts[:, 1] if p.axis == 0 else pts[:, 0]
+            s = pts[:, 0] if p.axis == 0 else pts[:, 1]
+            if target:
+                f = np.exp(p.decay_t[None, :] * (w[:, None] - p.shift_t[None, :])) * np.exp(1j * p.phase * s[:, None])
+            else:
+                f = np.exp(p.decay_s[None, :] * (w[:, None] - p.shift_s[None, :])) * np.exp(-1j * p.phase * s[:, None])
+            out.append(f)
+        return np.concatenate(out, axis=1)
+
+    def coeff_buffer(self):
+        return self.torch.zeros(2 * self.nmodes + 1, dtype=self.torch.float64)
+
+    def far_source(self, lo, hi, coeff):
+        S = self._mode_factors(self.src[lo:hi], False)
+        raw = S.T @ self.q[lo:hi]
+        moment = np.sum(self.src[lo:hi, 1] * self.q[lo:hi])
+        coeff[:] = self.torch.from_numpy(np.concatenate([raw.real, raw.imag, [moment]]))
+
+    def far_target(self, coeff, lo, hi):
+        c = coeff.numpy()
+        raw = c[:self.nmodes] + 1j * c[self.nmodes:2 * self.nmodes]
+        diag = np.concatenate([p.tables[0][0::2] + 1j * p.tables[0][1::2] for p in self.parts])
+        T = self._mode_factors(self.src[lo:hi], True)
+        u = T @ (diag * raw)
+        m0 = sum(p.m0[0] for p in self.parts if p.has_m0)
+        u = u + m0 * self.src[lo:hi, 1] * c[-1]
+        from types import SimpleNamespace
+
+        return SimpleNamespace(scalar=self.torch.from_numpy(np.ascontiguousarray(u.real)), velocity=None)
+
+    def _items(self):
+        nb = (self.n + TILE - 1) // TILE
+        items = []
+        for I in range(nb):
+            for J0 in range(I, nb, CHUNK):
+                items.append((I, J0, min(nb, J0 + CHUNK)))
+        return items
+
+    def near_items(self):
+        return len(self._items()), 1
+
+    def accumulator(self, n):
+        return self.torch.zeros(n, dtype=self.torch.int64)
+
+    def _G(self, t, s, identity_skip):
+        g = 0.0
+        for k, (sx, sy) in enumerate(self.shifts):
+            rx, ry = (t[0] - s[0]) - sx, (t[1] - s[1]) - sy
+            if rx == 0.0 and ry == 0.0:
+                assert identity_skip and k == self.ident
+                continue
+            g += -np.log(rx * rx + ry * ry) / (4 * np.pi)
+        return g
+
+    def near_partial(self, lo, hi, acc):
+        a = acc.numpy().reshape(-1, 1, 3)
+        for I, J0, J1 in self._items()[lo:hi]:
+            rows = range(I * TILE, min(self.n, (I + 1) * TILE))
+            racc = {l: 0.0 for l in rows}
+            for J in range(J0, J1):
+                cols = range(J * TILE, min(self.n, (J + 1) * TILE))
+                cacc = {j: 0.0 for j in cols}
+                for l in rows:
+                    for j in cols:
+                        if J == I:
+                            racc[l] += self.q[j] * self._G(self.src[l], self.src[j], True)
+                        elif True:
+                            g = self._G(self.src[l], self.src[j], False)
+                            racc[l] += self.q[j] * g
+                            cacc[j] += self.q[l] * g
+                if J != I:
+                    for j, v in cacc.items():
+                        a[j, 0] += _fx_split(np.float64(v))
+            for l, v in racc.items():
+                a[l, 0] += _fx_split(np.float64(v))
+
+    def fixed_to_out(self, acc, n, out):
+        v = _fx_value(acc.numpy().reshape(-1, 3)[:n])
+        out.scalar += self.torch.from_numpy(v)
+
+    def near_targets(self, lo, hi, out):
+        raise AssertionError("symmetric path expected")
+
+
+def _system(pw):
+    rng = np.random.default_rng(5)
+    n = 37  # not a multiple of the world size or the tile
+    src = np.ascontiguousarray(np.stack([rng.uniform(-0.5, 0.5, n), rng.uniform(-0.5, 0.5, n)], 1))
+    q = rng.uniform(-1, 1, n)
+    q -= q.mean()
+    cell = pw.make_unit_cell(1.0, 0.0, 1.0)
+    pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-6)
+    return pz, src, q
+
+
+def _worker(rank, world, port, outdir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2111_01083_b200 as pw
+    from paper_2111_01083_b200 import dist as pdist
+
+    pz, src, q = _system(pw)
+    be = NumpyBackend(pw, pz, src, q)
+    plan = pdist.ShardPlan(len(src), len(src), world, rank)
+    out, (lo, hi) = pdist.sharded_total_field(be, pdist.Comm(world), plan, symmetric=True)
+    np.save(os.path.join(outdir, f"r{rank}.npy"), np.concatenate([[lo, hi], out.scalar.numpy()]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_partitions_cover_everything():
+    from paper_2111_01083_b200 import dist as pdist
+
+    for n in (0, 1, 7, 37, 1000):
+        for world in (1, 2, 3, 8):
+            got = []
+            for r in range(world):
+                lo, hi = pdist.contiguous(n, world, r)
+                got.extend(range(lo, hi))
+            assert got == list(range(n))
+            got = []
+            for r in range(world):
+                lo, hi = pdist.target_slice(n, world, r)
+                assert hi - lo <= pdist.target_chunk(n, world)
+                got.extend(range(lo, hi))
+            assert got == list(range(n))
+
+
+def test_item_counts_match_the_device_decomposition(pw):
+    cell = pw.make_unit_cell(1.0, 0.0, 1.0, pw.Periodicity.Singly)
+    pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-10)
+    for n, want in ((1, 1), (512, 1), (513, 2), (1000000, None)):
+        items, nout = pw.near_sym_items(pz, n)
+        nb = (n + 511) // 512  # Laplace: 4 targets x 128 threads per tile, 8 tiles per item
+        assert items == sum((nb - i + 7) // 8 for i in range(nb))
+        assert nout == 1
+        if want is not None:
+            assert items == want
+    st = pw.make_periodizer(pw.Pde.Stokes, 0.0, pw.make_unit_cell(1.0, 0.0, 1.0), 1e-8)
+    assert pw.near_sym_items(st, 300, pw.ApplyOptions(with_pressure=True))[1] == 3
+
+
+def test_two_ranks_gloo_equal_one_rank(pw, port, tmp_path):
+    import torch.multiprocessing as mp
+
+    from paper_2111_01083_b200 import dist as pdist
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    parts = [np.load(tmp_path / f"r{r}.npy") for r in range(world)]
+    two = np.concatenate([p[2:] for p in parts])
+    assert [(int(p[0]), int(p[1])) for p in parts] == [pdist.target_slice(37, 2, r) for r in range(2)]
+
+    pz, src, q = _system(pw)
+    be = NumpyBackend(pw, pz, src, q)
+    one, _ = pdist.sharded_total_field(be, pdist.Comm(1), pdist.ShardPlan(37, 37, 1, 0), symmetric=True)
+    one = one.scalar.numpy()
+    # the Poisson far field carries ~1e9 weights on the lambda -> 0 modes, so a different
+    # summation order of the all-reduce moves the gauge constant: compare mean-removed
+    d = (two - two.mean()) - (one - one.mean())
+    assert np.max(np.abs(d)) <= 1e-13 * np.max(np.abs(one))
+    # against the direct sums: C restatement near images + the NumPy far field
+    from oracle.pyoracle import near_shifts
+
+    shifts, ident = near_shifts((1.0, 0.0, 1.0, 2))
+    near, _ = port.near(port.LAPLACE, src, src, shifts, ident, q=q)
+    coeff = be.coeff_buffer()
+    be.far_source(0, 37, coeff)
+    far = be.far_target(coeff, 0, 37).scalar.numpy()
+    want = near[:, 0] + far
+    assert np.max(np.abs(one - want)) <= 1e-12 * np.max(np.abs(want))
+    # the near part alone is exact integer arithmetic: two ranks == one rank bitwise
+    be2 = NumpyBackend(pw, pz, src, q)
+    items, _ = be2.near_items()
+    full = be2.accumulator(37 * 3)
+    be2.near_partial(0, items, full)
+    halves = be2.accumulator(37 * 3)
+    for r in range(2):
+        lo, hi = pdist.contiguous(items, 2, r)
+        part = be2.accumulator(37 * 3)
+        be2.near_partial(lo, hi, part)
+        halves += part
+    assert np.array_equal(full.numpy(), halves.numpy())

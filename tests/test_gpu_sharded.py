@@ -1,0 +1,80 @@
+"""Sharded passes on one GPU, run one after another (no kernel waits on another):
+the pieces a multi-GPU rank runs compose to the single-call result."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,n,pressure", [("c4", 30000, False), ("c3", 8000, True), ("c5", 12000, False)])
+def test_symmetric_items_compose_bitwise(pw, gpu, name, n, pressure):
+    import torch
+
+    from paper_2111_01083_b200 import configs, dist as pdist
+
+    inp = configs.generate(name, n_src=n)
+    c = inp.config
+    pz = pw.make_periodizer(c.pde, c.beta, pw.make_unit_cell(*c.cell[:3], c.cell[3]), c.eps)
+    kw = "charges" if c.strength == "charge" else "forces"
+    src = torch.from_numpy(inp.sources).cuda()
+    q = torch.from_numpy(inp.charges if kw == "charges" else inp.forces).cuda()
+    opt = pw.ApplyOptions(with_pressure=pressure)
+    whole = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **{kw: q}), opt)
+    items, nout = pw.near_sym_items(pz, n, opt)
+    for world in (2, 3):
+        acc = torch.zeros(n * nout * 3, dtype=torch.int64, device="cuda")
+        for r in range(world):
+            lo, hi = pdist.contiguous(items, world, r)
+            part = torch.zeros_like(acc)
+            pw.near_sym_partial(pz, pw.ParticleSystem(sources=src, targets=src, **{kw: q}), part, lo, hi, opt)
+            acc += part  # the int64 reduce-scatter operand
+        got = pw.FieldResult()
+        key = "scalar" if kw == "charges" else "velocity"
+        setattr(got, key, torch.zeros_like(getattr(whole, key)))
+        if pressure:
+            got.pressure = torch.zeros_like(whole.pressure)
+        pw.fixed_to_field(pz, acc, n, got, opt, like=src)
+        assert torch.equal(getattr(got, key), getattr(whole, key))
+        if pressure:
+            assert torch.equal(got.pressure, whole.pressure)
+
+
+def test_sharded_total_field_matches_single_call(pw, gpu):
+    """dist.sharded_total_field with a single-process Comm per simulated rank; the
+    all-reduce / reduce-scatter are done by summing the per-rank buffers here."""
+    import torch
+
+    from paper_2111_01083_b200 import configs, dist as pdist
+
+    inp = configs.generate("c4", n_src=20001)
+    c = inp.config
+    pz = pw.make_periodizer(c.pde, c.beta, pw.make_unit_cell(*c.cell[:3], c.cell[3]), c.eps)
+    src = torch.from_numpy(inp.sources).cuda()
+    q = torch.from_numpy(inp.charges).cuda()
+    opt = pw.ApplyOptions()
+    ref = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=src, charges=q), opt)
+    n, world = 20001, 3
+    be = pdist.CudaBackend(pw, pz, opt, src, q, "charges")
+    coeff = be.coeff_buffer()
+    for r in range(world):
+        part = be.coeff_buffer()
+        be.far_source(*pdist.contiguous(n, world, r), part)
+        coeff += part
+    items, nout = be.near_items()
+    chunk = pdist.target_chunk(n, world)
+    acc = be.accumulator(chunk * world * nout * 3)
+    for r in range(world):
+        part = be.accumulator(chunk * world * nout * 3)
+        be.near_partial(*pdist.contiguous(items, world, r), part)
+        acc += part
+    outs = []
+    for r in range(world):
+        lo, hi = pdist.target_slice(n, world, r)
+        out = be.far_target(coeff, lo, hi)
+        assert out.accelerated == ref.accelerated
+        be.fixed_to_out(acc[r * chunk * nout * 3:(r + 1) * chunk * nout * 3], hi - lo, out)
+        outs.append(out.scalar)
+    got = torch.cat(outs).cpu().numpy()
+    assert rel_l2(got, ref.scalar.cpu().numpy(), gauge=True) <= 1e-13
