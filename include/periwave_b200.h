@@ -215,6 +215,17 @@ int pwb_fixed_to_field(const pwb_periodizer* pz, const pwb_options* opt, const i
  * evaluated on the device for device-resident systems. */
 int pwb_validate(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt);
 
+/* ------------------------------------------------------------ validation tools (GPU)
+ * brute_force_far (proj/src/oracle.cpp:83-110, oracle.hpp:30-31): shell-by-shell
+ *   +-paired lattice sum of the images outside the near set (each image one GPU
+ *   accumulate launch), early stop after 3 quiet shells; overwrites *out. Host memory.
+ * periodicity_residual (proj/src/oracle.cpp:112-173, oracle.hpp:43-44): face jumps of
+ *   total_field over samples_per_side points per face; the system's targets are ignored. */
+int pwb_brute_force_far(const pwb_periodizer* pz, const pwb_system* sys, int shells, const pwb_options* opt,
+                        pwb_field* out);
+int pwb_periodicity_residual(const pwb_periodizer* pz, const pwb_system* sys, int samples_per_side,
+                             const pwb_options* opt, double* e1, double* e2, double* scale);
+
 /* ------------------------------------------------------------ NUFFT
  * nufft_type1/2/3 (proj/src/nufft.cpp:71-82, nufft.hpp:21-31). Complex arrays
  * interleaved; `memory` applies to every array argument. */

@@ -133,7 +133,8 @@ EXPORTED = [
     "pwb_far_coeff_size", "pwb_far_source_pass", "pwb_far_target_pass", "pwb_validate",
     "pwb_nufft_type1", "pwb_nufft_type2", "pwb_nufft_type3", "pwb_fast_nufft_available",
     "pwb_eval_kernel", "pwb_rng_uniform", "pwb_launch_count", "pwb_last_phase_ms", "pwb_fp64_peak_probe",
-    "pwb_near_sym_items", "pwb_near_sym_partial", "pwb_fixed_to_field",
+    "pwb_near_sym_items", "pwb_near_sym_partial", "pwb_fixed_to_field", "pwb_brute_force_far",
+    "pwb_periodicity_residual",
 ]
 
 _lib = None
@@ -190,6 +191,10 @@ def lib() -> ctypes.CDLL:
     L.pwb_near_sym_partial.argtypes = [vp, ctypes.POINTER(_System), ctypes.POINTER(_Options), ctypes.c_long,
                                        ctypes.c_long, vp]
     L.pwb_fixed_to_field.argtypes = [vp, ctypes.POINTER(_Options), vp, sz, ctypes.POINTER(_Field)]
+    L.pwb_brute_force_far.argtypes = [vp, ctypes.POINTER(_System), i, ctypes.POINTER(_Options),
+                                      ctypes.POINTER(_Field)]
+    L.pwb_periodicity_residual.argtypes = [vp, ctypes.POINTER(_System), i, ctypes.POINTER(_Options),
+                                           ctypes.POINTER(d), ctypes.POINTER(d), ctypes.POINTER(d)]
     _lib = L
     return L
 
@@ -627,6 +632,33 @@ def far_target_pass(pz: Periodizer, sys: ParticleSystem, coeff, opt: Optional[Ap
                                      coeff.data_ptr(), ctypes.byref(f)))
     res.accelerated = bool(f.accelerated)
     return res
+
+
+def brute_force_far(pz: Periodizer, sys: ParticleSystem, shells: int,
+                    opt: Optional[ApplyOptions] = None) -> FieldResult:
+    """Shell-by-shell lattice sum of the far images (reference oracle.cpp:83-110), on the GPU."""
+    opt = opt or ApplyOptions()
+    s, mem = sys._c()
+    if mem != MEM_HOST:
+        raise ValueError("brute_force_far takes host arrays")
+    res, f = _field_for(pz, opt, s.n_tgt, False, None, None)
+    o = opt._c()
+    _check(lib().pwb_brute_force_far(pz.handle, ctypes.byref(s), int(shells), ctypes.byref(o), ctypes.byref(f)))
+    return res
+
+
+def periodicity_residual(pz: Periodizer, sys: ParticleSystem, samples_per_side: int,
+                         opt: Optional[ApplyOptions] = None) -> dict:
+    """Face-jump residual of total_field (reference oracle.cpp:112-173): {e1, e2, scale, rel}."""
+    s, mem = sys._c()
+    if mem != MEM_HOST:
+        raise ValueError("periodicity_residual takes host arrays")
+    e1, e2, sc = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    o = (opt or ApplyOptions())._c()
+    _check(lib().pwb_periodicity_residual(pz.handle, ctypes.byref(s), int(samples_per_side), ctypes.byref(o),
+                                          ctypes.byref(e1), ctypes.byref(e2), ctypes.byref(sc)))
+    rel = max(e1.value, e2.value) / max(sc.value, 1e-300)
+    return {"e1": e1.value, "e2": e2.value, "scale": sc.value, "rel": rel}
 
 
 def near_sym_items(pz: Periodizer, n: int, opt: Optional[ApplyOptions] = None):

@@ -654,6 +654,75 @@ int pwb_far_target_pass(const pwb_periodizer* h, const pwb_system* s, const pwb_
   });
 }
 
+namespace {
+periwave::ParticleSystem host_system(const pwb_system* s) {
+  auto v2 = [](const double* p, size_t n) {
+    std::vector<periwave::Vec2> v(p ? n : 0);
+    for (size_t i = 0; i < v.size(); ++i) v[i] = {p[2 * i], p[2 * i + 1]};
+    return v;
+  };
+  periwave::ParticleSystem ps;
+  ps.sources = v2(s->sources, s->n_src);
+  if (s->charges) ps.charges.assign(s->charges, s->charges + s->n_src);
+  ps.forces = v2(s->forces, s->n_src);
+  ps.normals = v2(s->normals, s->n_src);
+  if (s->coefficients)
+    for (size_t i = 0; i < s->n_src; ++i) ps.coefficients.emplace_back(s->coefficients[2 * i], s->coefficients[2 * i + 1]);
+  ps.targets = v2(s->targets, s->n_tgt);
+  return ps;
+}
+
+periwave::ApplyOptions api_options(const pwb_options* o) {
+  periwave::ApplyOptions a;
+  if (!o) return a;
+  a.path = o->path == PWB_PATH_DIRECT ? periwave::ApplyPath::Direct
+           : o->path == PWB_PATH_ACCELERATED ? periwave::ApplyPath::Accelerated
+                                             : periwave::ApplyPath::Auto;
+  a.threads = o->threads;
+  a.with_pressure = o->with_pressure != 0;
+  a.nufft_eps = o->nufft_eps;
+  a.with_gradient = o->with_gradient != 0;
+  a.device = o->device;
+  a.stream = o->stream;
+  return a;
+}
+}  // namespace
+
+int pwb_brute_force_far(const pwb_periodizer* h, const pwb_system* s, int shells, const pwb_options* o,
+                        pwb_field* f) {
+  if (!h || !s || !f) return fail_arg("null argument");
+  if (s->memory != PWB_MEM_HOST || f->memory != PWB_MEM_HOST) return fail_arg("validation tools take host memory");
+  return guard([&] {
+    const periwave::FieldResult r = periwave::brute_force_far(h->pz, host_system(s), shells, api_options(o));
+    const size_t nt = s->n_tgt;
+    if (f->scalar && r.scalar.size() == nt) std::copy(r.scalar.begin(), r.scalar.end(), f->scalar);
+    if (f->velocity && r.velocity.size() == nt)
+      for (size_t i = 0; i < nt; ++i) {
+        f->velocity[2 * i] = r.velocity[i].x;
+        f->velocity[2 * i + 1] = r.velocity[i].y;
+      }
+    if (f->complex_scalar && r.complex_scalar.size() == nt)
+      for (size_t i = 0; i < nt; ++i) {
+        f->complex_scalar[2 * i] = r.complex_scalar[i].real();
+        f->complex_scalar[2 * i + 1] = r.complex_scalar[i].imag();
+      }
+    return OK;
+  });
+}
+
+int pwb_periodicity_residual(const pwb_periodizer* h, const pwb_system* s, int samples, const pwb_options* o,
+                             double* e1, double* e2, double* scale) {
+  if (!h || !s || !e1 || !e2 || !scale) return fail_arg("null argument");
+  if (s->memory != PWB_MEM_HOST) return fail_arg("validation tools take host memory");
+  return guard([&] {
+    const periwave::ResidualReport r = periwave::periodicity_residual(h->pz, host_system(s), samples, api_options(o));
+    *e1 = r.e1;
+    *e2 = r.e2;
+    *scale = r.scale;
+    return OK;
+  });
+}
+
 int pwb_near_sym_items(const pwb_periodizer* h, size_t n, const pwb_options* o, long* n_items, int* nout) {
   if (!h || !n_items) return fail_arg("null argument");
   return guard([&] {

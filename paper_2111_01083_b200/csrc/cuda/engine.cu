@@ -957,7 +957,9 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   a.flag = flag;
   const size_t nout = near_outputs(nk);
   // targets == sources (same array): every unordered pair once (near_sym.cu)
-  const bool symmetric = !single && s.tgt == s.src && s.nt == s.ns && s.nt >= 512 && near_sym_supported(nk) &&
+  // (below ~32K points the triangle has too few work items to fill 148 SMs; the
+  // one-sided tile with source splits is faster there)
+  const bool symmetric = !single && s.tgt == s.src && s.nt == s.ns && s.nt >= 32768 && near_sym_supported(nk) &&
                          std::getenv("PWB_NO_SYMMETRIC") == nullptr;
   cuda_check(cudaEventRecord(ev_[2], st), "event");
   bool done = false;

@@ -447,14 +447,14 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   const size_t want = static_cast<size_t>(sm_count) * 4;
   if (bx < want && partial_ws != nullptr) {
     splits = static_cast<int>((want + bx - 1) / bx);
-    const size_t max_by_src = (a.ns + 4 * kTile - 1) / (4 * kTile);
+    const size_t max_by_src = (a.ns + 63) / 64;  // >= 64 sources per split
     if (static_cast<size_t>(splits) > max_by_src) splits = static_cast<int>(max_by_src);
     if (splits > kMaxSplits) splits = kMaxSplits;
     if (splits < 1) splits = 1;
   }
   a.splits = splits;
   a.src_per_split = (a.ns + splits - 1) / splits;
-  a.src_per_split = ((a.src_per_split + kTile - 1) / kTile) * kTile;
+  a.src_per_split = ((a.src_per_split + 7) / 8) * 8;
   a.partial = partial_ws;
   dim3 grid(bx, splits);
   near_tile_kernel<KER, NXI, NROW, TPT><<<grid, kThreads, 0, st>>>(a);

@@ -322,7 +322,7 @@ def test_sharded_far_equals_unsharded(pw, gpu):
 
 
 # ------------------------------------------------------------------ symmetric tile (targets == sources)
-@pytest.mark.parametrize("name,n", [("c1", 1000), ("c3", 3000), ("c4", 5000), ("c5", 4000)])
+@pytest.mark.parametrize("name,n", [("c1", 1000), ("c3", 33000), ("c4", 40000), ("c5", 33000)])
 def test_symmetric_targets_equal_sources(pw, gpu, ref, name, n):
     """targets given as the sources array -> every unordered pair evaluated once (near_sym.cu)."""
     from paper_2111_01083_b200 import configs
@@ -349,14 +349,14 @@ def test_symmetric_targets_equal_sources(pw, gpu, ref, name, n):
 def test_symmetric_gradient_and_pressure(pw, gpu, ref):
     rng = np.random.default_rng(77)
     cellt = (1.0, 0.3, 0.8, 2)
-    src, _, kw = _system(rng, cellt, 2000, 1, "charge", False)
+    src, _, kw = _system(rng, cellt, 33000, 1, "charge", False)
     pz = pw.make_periodizer(pw.Pde.ModHelmholtz, 10.0, _cell(pw, cellt), 1e-10)
     opt = pw.ApplyOptions(path=pw.ApplyPath.Direct, with_gradient=True)
     a = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw), opt)
     b = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), **kw), opt)
     assert rel_l2(a.scalar, b.scalar) <= 1e-14 and rel_l2(a.gradient, b.gradient) <= 1e-14
     cellt = (1.0, 0.0, 1.0, 2)
-    src, _, kw = _system(rng, cellt, 2000, 1, "force", True)
+    src, _, kw = _system(rng, cellt, 33000, 1, "force", True)
     pz = pw.make_periodizer(pw.Pde.Stokes, 0.0, _cell(pw, cellt), 1e-8)
     opt = pw.ApplyOptions(path=pw.ApplyPath.Direct, with_pressure=True)
     a = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw), opt)
