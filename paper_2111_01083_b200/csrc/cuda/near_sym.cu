@@ -36,6 +36,9 @@
 namespace pwb {
 namespace {
 
+#ifndef PWB_SYM_LAPLACE_MINB
+#define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM: 80-register cap (ncu r1: 94 regs -> 20 warps)
+#endif
 constexpr int kT = 128;  // threads per block
 constexpr int kWarps = kT / 32;
 
@@ -78,7 +81,7 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
 // values_fast(): branch-free, only valid when `bad` stays 0 (FAST kernels).
 
 struct SymLaplace {
-  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = 4, CHUNK = 8;
+  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = 4, CHUNK = 8, MINB = PWB_SYM_LAPLACE_MINB;
   static constexpr bool FAST = true;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -127,7 +130,7 @@ struct SymLaplace {
 
 template <bool GRAD>
 struct SymModHelm {
-  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16;
+  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0;
   static constexpr bool FAST = false;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const pwk::LogK&,
@@ -190,7 +193,7 @@ struct SymModHelm {
 template <bool PRESSURE>
 struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
-                       CHUNK = 16;
+                       CHUNK = 16, MINB = 0;
   static constexpr bool FAST = true;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -297,7 +300,7 @@ __device__ __forceinline__ void load_w(const NearArgs& a, size_t j, bool live, d
 }
 
 template <class K, int NXI, int NROW>
-__global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
+__device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   constexpr int TPT = K::TPT;
   constexpr int TILE = kT * TPT;
   const NearArgs& a = S.a;
@@ -467,6 +470,21 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
   }
 }
 
+
+// K::MINB > 0 caps registers for K::MINB resident blocks per SM (one image row; the 2-D
+// image blocks hold more live shifts and get at most 4 -- 80 or 96 regs spill there).
+// MINB == 0 keeps ptxas's own allocation (the wider functors).
+template <class K, int NXI, int NROW>
+__global__ void __launch_bounds__(kT, NROW == 1 ? K::MINB : (K::MINB < 4 ? K::MINB : 4))
+    near_sym_kernel_capped(const __grid_constant__ SymArgs S) {
+  near_sym_body<K, NXI, NROW>(S);
+}
+
+template <class K, int NXI, int NROW>
+__global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
+  near_sym_body<K, NXI, NROW>(S);
+}
+
 template <class K, int NXI, int NROW>
 void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
                       int* row_start_host, const SymRange& range) {
@@ -495,7 +513,10 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
   S.fx = fx;
   S.item0 = static_cast<int>(b);
   if (e > b) {
-    near_sym_kernel<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
+    if constexpr (K::MINB > 0)
+      near_sym_kernel_capped<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
+    else
+      near_sym_kernel<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
     count_launches(1);
   }
   if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, st);
