@@ -222,7 +222,7 @@ int run(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, pwb_
     std::lock_guard<std::mutex> lock(p.mutex());
     pwb::Opts opt = opts_from(o);
     try {
-      check_outputs(h->pz, opt, f);
+      if (s->n_tgt > 0) check_outputs(h->pz, opt, f);  // no targets: empty result, validation still runs
     } catch (const std::invalid_argument& e) {
       return fail_arg(e.what());
     }

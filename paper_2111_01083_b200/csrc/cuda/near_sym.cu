@@ -37,7 +37,7 @@ namespace pwb {
 namespace {
 
 #ifndef PWB_SYM_LAPLACE_MINB
-#define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM: 80-register cap (ncu r1: 94 regs -> 20 warps)
+#define PWB_SYM_LAPLACE_MINB 5  // 5 x 4 warps/SM (96 regs); 6 (80 regs) spills and measured 1.1 % slower on c4
 #endif
 constexpr int kT = 128;  // threads per block
 constexpr int kWarps = kT / 32;

@@ -190,6 +190,7 @@ def test_apply_matches_reference_and_wraps(cli, gpu, ref, tmp_path, pde, beta, c
             w -= w.mean(axis=0)
     else:
         f = rng.uniform(-1, 1, (n, 2))
+        f -= f.mean(axis=0)  # the double-layer periodizer also requires neutral densities
         ang = rng.uniform(0, 2 * np.pi, n)
         w = np.concatenate([f, np.stack([np.cos(ang), np.sin(ang)], 1)], 1)
     src, tgt, out = tmp_path / "s.txt", tmp_path / "t.txt", tmp_path / "o.txt"

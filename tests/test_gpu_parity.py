@@ -354,7 +354,8 @@ def test_symmetric_gradient_and_pressure(pw, gpu, ref):
     opt = pw.ApplyOptions(path=pw.ApplyPath.Direct, with_gradient=True)
     a = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw), opt)
     b = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), **kw), opt)
-    assert rel_l2(a.scalar, b.scalar) <= 1e-14 and rel_l2(a.gradient, b.gradient) <= 1e-14
+    # summation order differs (one-sided fp64 vs fixed-point symmetric): agreement ~1e-14
+    assert rel_l2(a.scalar, b.scalar) <= 1e-13 and rel_l2(a.gradient, b.gradient) <= 1e-13
     cellt = (1.0, 0.0, 1.0, 2)
     src, _, kw = _system(rng, cellt, 33000, 1, "force", True)
     pz = pw.make_periodizer(pw.Pde.Stokes, 0.0, _cell(pw, cellt), 1e-8)
