@@ -941,9 +941,54 @@ void Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, uns
 void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, const DevOut& out) {
   NearArgs a;
   near_args(DevSys{}, o, out, false, 0, 0, false, a);
-  launch_fx_finish(acc, n, a.out0, a.nout0, a.out1, a.nout1, stream_for(o));
+  launch_fx_finish(acc, n, a.out0, a.nout0, a.out1, a.nout1, nullptr, stream_for(o));
   cuda_check(cudaGetLastError(), "fixed-point finish");
   cuda_check(cudaStreamSynchronize(stream_for(o)), "sync");
+}
+
+// Morton-ordered copies of the points and strengths; outputs keep their original
+// rows through a.out_row (binning.cu explains why the screened kernels want this).
+void Plan::bin_inputs(const DevSys& s, NearArgs& a, cudaStream_t st) {
+  const periwave::UnitCell& c = pz_.cell;
+  const double wx = c.d + std::abs(c.xi), wy = c.eta;
+  BinBox box;
+  box.x0 = -0.5 * wx;
+  box.y0 = -0.5 * wy;
+  box.inv_h = 65535.0 / std::max(wx, wy);
+  const bool same = a.tgt == a.src;
+  const size_t ws_bytes = morton_order_bytes(std::max(s.ns, s.nt));
+  void* ws = bin_ws_.ensure(ws_bytes);
+  int* ps = bin_perm_s_.as<int>(s.ns);
+  morton_order(a.src, s.ns, box, ps, ws, ws_bytes, st);
+  double2* src = bin_src_.as<double2>(s.ns);
+  gather_double2(a.src, ps, s.ns, src, st);
+  if (a.q) {
+    double* q = bin_q_.as<double>(s.ns);
+    gather_double(a.q, ps, s.ns, q, st);
+    a.q = q;
+  }
+  if (a.vec) {
+    double2* v = bin_vec_.as<double2>(s.ns);
+    gather_double2(a.vec, ps, s.ns, v, st);
+    a.vec = v;
+  }
+  if (a.nrm) {
+    double2* v = bin_nrm_.as<double2>(s.ns);
+    gather_double2(a.nrm, ps, s.ns, v, st);
+    a.nrm = v;
+  }
+  if (same) {
+    a.tgt = src;
+    a.out_row = ps;
+  } else {
+    int* pt = bin_perm_t_.as<int>(s.nt);
+    morton_order(a.tgt, s.nt, box, pt, ws, ws_bytes, st);
+    double2* tgt = bin_tgt_.as<double2>(s.nt);
+    gather_double2(a.tgt, pt, s.nt, tgt, st);
+    a.tgt = tgt;
+    a.out_row = pt;
+  }
+  a.src = src;
 }
 
 void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
@@ -962,6 +1007,11 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   const bool symmetric = !single && s.tgt == s.src && s.nt == s.ns && s.nt >= 32768 && near_sym_supported(nk) &&
                          std::getenv("PWB_NO_SYMMETRIC") == nullptr;
   cuda_check(cudaEventRecord(ev_[2], st), "event");
+  // screened kernels branch on beta*r per pair: bin so the branch is warp-uniform
+  const bool screened = nk == NearKind::ModHelm || nk == NearKind::ModHelmGrad || nk == NearKind::ModStokes ||
+                        nk == NearKind::ModStokesP || (nk == NearKind::Multipole && a.screened);
+  if (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)
+    bin_inputs(s, a, st);
   bool done = false;
   if (symmetric) {
     const size_t nb = near_sym_tiles(s.nt);

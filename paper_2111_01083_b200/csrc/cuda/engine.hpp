@@ -182,6 +182,9 @@ class Plan {
   PinnedBuf host_checks_;
   DevBuf sym_fx_, sym_rows_;
   PinnedBuf sym_rows_host_;
+  // spatially binned copies of the near-field inputs (binning.cu)
+  DevBuf bin_ws_, bin_perm_s_, bin_perm_t_, bin_src_, bin_tgt_, bin_q_, bin_vec_, bin_nrm_;
+  void bin_inputs(const DevSys& s, NearArgs& a, cudaStream_t st);
   std::mutex mu_;
   cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
   bool far_timed_ = false, near_timed_ = false;

@@ -411,9 +411,10 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
     double o[KER::NOUT];
     KER::finish(acc[k], a, o);
     if (a.splits == 1) {
+      const size_t row = a.out_row ? static_cast<size_t>(a.out_row[l]) : l;
 #pragma unroll
       for (int c = 0; c < KER::NOUT; ++c) {
-        double* dst = c < a.nout0 ? a.out0 + l * a.nout0 + c : a.out1 + l * a.nout1 + (c - a.nout0);
+        double* dst = c < a.nout0 ? a.out0 + row * a.nout0 + c : a.out1 + row * a.nout1 + (c - a.nout0);
         *dst += o[c];
       }
     } else {
@@ -426,14 +427,15 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
 
 // out += sum_split partial[split] in fixed split order.
 __global__ void near_reduce_kernel(const double* partial, int splits, size_t nt, int nout, double* out0, int nout0,
-                                   double* out1, int nout1) {
+                                   double* out1, int nout1, const int* out_row) {
   const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= nt * nout) return;
   const size_t l = idx / nout;
   const int c = static_cast<int>(idx % nout);
   double s = 0.0;
   for (int sp = 0; sp < splits; ++sp) s += partial[static_cast<size_t>(sp) * nt * nout + idx];
-  double* dst = c < nout0 ? out0 + l * nout0 + c : out1 + l * nout1 + (c - nout0);
+  const size_t row = out_row ? static_cast<size_t>(out_row[l]) : l;
+  double* dst = c < nout0 ? out0 + row * nout0 + c : out1 + row * nout1 + (c - nout0);
   *dst += s;
 }
 
@@ -462,7 +464,7 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   if (splits > 1) {
     const size_t n = a.nt * KER::NOUT;
     near_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(partial_ws, splits, a.nt, KER::NOUT,
-                                                                               a.out0, a.nout0, a.out1, a.nout1);
+                                                                               a.out0, a.nout0, a.out1, a.nout1, a.out_row);
     count_launches(1);
   }
 }

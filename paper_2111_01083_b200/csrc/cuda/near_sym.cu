@@ -59,7 +59,7 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
 }
 
 __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double* out0, int nout0, double* out1,
-                                 int nout1) {
+                                 int nout1, const int* out_row) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int nout = nout0 + nout1;
   if (i >= n * nout) return;
@@ -68,7 +68,7 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
   const long long c = static_cast<long long>(acc[3 * i + 2]);
   const double v = fma(static_cast<double>(a), 0x1p22,
                        fma(static_cast<double>(b), 0x1p-20, static_cast<double>(c) * 0x1p-62));
-  const size_t l = i / nout;
+  const size_t l = out_row ? static_cast<size_t>(out_row[i / nout]) : i / nout;
   const int k = static_cast<int>(i % nout);
   double* dst = k < nout0 ? out0 + l * nout0 + k : out1 + l * nout1 + (k - nout0);
   *dst += v;
@@ -519,7 +519,7 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
       near_sym_kernel<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
     count_launches(1);
   }
-  if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, st);
+  if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, a.out_row, st);
 }
 
 template <class K>
@@ -535,10 +535,11 @@ bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, in
 }  // namespace
 
 void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int nout0, double* out1, int nout1,
-                      cudaStream_t st) {
+                      const int* out_row, cudaStream_t st) {
   const size_t total = n * static_cast<size_t>(nout0 + nout1);
   if (total == 0) return;
-  fx_finish_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(fx, n, out0, nout0, out1, nout1);
+  fx_finish_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(fx, n, out0, nout0, out1, nout1,
+                                                                               out_row);
   count_launches(1);
 }
 

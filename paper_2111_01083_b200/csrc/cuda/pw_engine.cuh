@@ -50,7 +50,19 @@ struct NearArgs {
   int splits = 1;
   size_t src_per_split = 0;
   int* flag = nullptr;     // set to 1 on a non-identity exact coincidence
+  const int* out_row = nullptr;  // binned targets: output row of target l (nullptr: l)
 };
+
+// ---------------------------------------------------------------- spatial binning (binning.cu)
+struct BinBox {  // uniform grid: cell = floor((p - (x0, y0)) * inv_h), 16 bits per axis
+  double x0 = 0.0, y0 = 0.0, inv_h = 1.0;
+};
+size_t morton_order_bytes(size_t n);
+// perm[i] = index of the i-th point in Morton order (stable in the input index).
+void morton_order(const double2* pts, size_t n, const BinBox& box, int* perm, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
+void gather_double(const double* in, const int* perm, size_t n, double* out, cudaStream_t st);
+void gather_double2(const double2* in, const int* perm, size_t n, double2* out, cudaStream_t st);
 
 size_t near_outputs(NearKind kind);
 void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count);
@@ -72,6 +84,7 @@ struct SymRange {
 bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
                      int* row_start_host, const SymRange& range);
 void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int nout0, double* out1, int nout1,
+                      const int* out_row,
                       cudaStream_t st);
 // host-only: number of work items of the symmetric decomposition (0 if none)
 long near_sym_item_count(NearKind kind, size_t n);

@@ -21,8 +21,15 @@ def test_symmetric_items_compose_bitwise(pw, gpu, name, n, pressure):
     src = torch.from_numpy(inp.sources).cuda()
     q = torch.from_numpy(inp.charges if kw == "charges" else inp.forces).cuda()
     opt = pw.ApplyOptions(with_pressure=pressure)
-    # n above the symmetric-tile threshold (32768), so the single call takes the same tile
-    whole = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **{kw: q}), opt)
+    # n above the symmetric-tile threshold (32768), so the single call takes the same tile;
+    # the sharded items run in input order, so the single call must not bin (binning.cu)
+    import os
+
+    os.environ["PWB_NO_BINNING"] = "1"
+    try:
+        whole = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **{kw: q}), opt)
+    finally:
+        del os.environ["PWB_NO_BINNING"]
     items, nout = pw.near_sym_items(pz, n, opt)
     for world in (2, 3):
         acc = torch.zeros(n * nout * 3, dtype=torch.int64, device="cuda")
