@@ -33,7 +33,32 @@ F_PAIR = {"c1": 29, "c2": 153, "c3": 48, "c4": 29, "c5": 94}
 F_FAR = {"c1": 70, "c2": 70, "c3": 86, "c4": 70, "c5": 70}
 # fp64-pipe instructions per (target, source) pair-group of the symmetric tile (all images),
 # counted in the SASS of the fast inner loop (cuobjdump; profiles/r1_c4_near_sym_ncu.md)
-FP64_INSTR_PER_GROUP = {"c4": 31.25}
+# (tools/sass_loop_stats.py), per log tier: the reduced tier runs when eps >= 1e-11 unless
+# PWB_FULL_LOG is set (pw_math.cuh log_pos_k)
+FP64_INSTR_PER_GROUP = {("c4", "full"): 29.25, ("c4", "reduced"): 25.25,
+                        ("c3", "full"): 135.0, ("c3", "reduced"): 122.0}
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_traffic.json")
+
+
+def near_kernel_name(config, symmetric):
+    """The dominant near launch of a config (engine.cu Plan::near, near.cu / near_sym.cu)."""
+    fam = {"c1": ("SymLaplace", "Laplace", "3,3"), "c2": ("SymModHelm<grad>", "ModHelmGrad", "5,3"),
+           "c3": ("SymStokes", "Stokes<no pressure>", "3,3"), "c4": ("SymLaplace", "Laplace", "3,1"),
+           "c5": ("SymModHelm", "ModHelm", "3,3")}[config]
+    binned = " on Morton-binned inputs" if config in ("c2", "c5") else ""
+    if symmetric:
+        return f"near_sym_kernel<{fam[0]},{fam[2]}> (fused near images, each unordered pair once){binned}"
+    return f"near_tile_kernel<{fam[1]},{fam[2]}> (fused near images){binned}"
+
+
+def measured_traffic(config, n):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture (same config, same N)."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f).get(config)
+    except (OSError, ValueError):
+        return None
+    return t["bytes"] if t and t.get("n") == n else None
 WORKLOAD = {
     "c1": "c1: doubly periodic Poisson, square cell, N=1000 uniform, targets=sources, eps=1e-10",
     "c2": "c2: doubly periodic mod. Helmholtz beta=10, cell (1,0.3,0.8), 1e5 src / 1e5 tgt, eps=1e-10, u+grad u",
@@ -363,9 +388,10 @@ def main():
     # (target, source) pair-group covering all images, profiles/r1_c4_near_sym_ncu.md) over the
     # DFMA instruction peak (peak TFLOP/s / 2)
     pipe_frac = None
-    if same and args.config in FP64_INSTR_PER_GROUP:
+    tier = "reduced" if (c.eps >= 1e-11 and not os.environ.get("PWB_FULL_LOG")) else "full"
+    if same and (args.config, tier) in FP64_INSTR_PER_GROUP and ws == 1:
         groups = ns * (ns + 1) / 2.0
-        pipe_frac = groups * FP64_INSTR_PER_GROUP[args.config] / (t_near * 1e-3) / (peak.value * 1e12 / 2.0)
+        pipe_frac = groups * FP64_INSTR_PER_GROUP[(args.config, tier)] / (t_near * 1e-3) / (peak.value * 1e12 / 2.0)
 
     line = None
     if rank == 0:
@@ -390,11 +416,10 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                         "frac": achieved / peak.value if peak.value else None, "traffic": None,
-                         "kernel": ("near_sym_kernel<SymLaplace,3,1> (fused near images, each unordered pair once)"
-                                    if same else "near_tile_kernel<Laplace,3,1,2> (fused near images)")
-                         if args.config == "c4"
-                         else "near_tile_kernel (fused near images)",
+                         "frac": achieved / peak.value if peak.value else None,
+                         "traffic": measured_traffic(args.config, ns) if ws == 1 else None,
+                         "log_tier": tier,
+                         "kernel": near_kernel_name(args.config, same and (ns >= 32768 or ws > 1)),
                          "near_ms_per_launch": t_near, "far_ms": t_step - t_near,
                          "fp64_pipe_frac": pipe_frac,
                          "note": "frac > 1: the fused symmetric tile evaluates each unordered (target, source)"

@@ -242,8 +242,10 @@ int pwb_fast_nufft_available(void);
  * Batch evaluation of the device functions the P2P tiles use (kernels.cpp:78-162),
  * for parity tests. which: 0 bessel_kn(l, x); 1 greens_scalar(pde, beta, r);
  * 2 greens_block (4 out); 3 multipole_kernel(pde, beta, l, r) (2 out);
- * 4 pressurelet (2 out); 5 stresslet_dlp(r, n) (4 out). Inputs per point:
- * which 0: x (1 double); 1-4: r (2); 5: r, n (4). Host memory. */
+ * 4 pressurelet (2 out); 5 stresslet_dlp(r, n) (4 out); 6 the symmetric tiles'
+ * ln(x) in both precision tiers + the MUFU reciprocal seed + the refined
+ * reciprocal of x (4 out, no reference counterpart). Inputs per point:
+ * which 0, 6: x (1 double); 1-4: r (2); 5: r, n (4). Host memory. */
 int pwb_eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out);
 
 /* ------------------------------------------------------------ measurement */

@@ -111,6 +111,17 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       out[4 * i + 3] = c * ry * ry;
       break;
     }
+    case 6: {  // the hot tiles' log tiers and reciprocal steps (pw_math.cuh)
+      const double x = in[i];
+      int bad = 0;
+      out[4 * i] = pwk::log_pos_k<false>(x, pwk::log_consts<false>(), bad);
+      out[4 * i + 1] = pwk::log_pos_k<true>(x, pwk::log_consts<true>(), bad);
+      double r;
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+      out[4 * i + 2] = r;
+      out[4 * i + 3] = pwk::rcp_fast(x);
+      break;
+    }
     default:
       out[i] = nan("");
   }
@@ -166,7 +177,7 @@ double fp64_peak_probe() {
   return best;
 }
 
-int eval_in_width(int which) { return which == 0 ? 1 : which == 5 ? 4 : 2; }
+int eval_in_width(int which) { return (which == 0 || which == 6) ? 1 : which == 5 ? 4 : 2; }
 int eval_out_width(int which) { return which <= 1 ? 1 : (which == 3 || which == 4) ? 2 : 4; }
 
 void run_eval(int which, int pde, double beta, int l, size_t n, const double* in_host, double* out_host) {

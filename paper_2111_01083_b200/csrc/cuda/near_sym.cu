@@ -80,12 +80,13 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
 // values():      careful per-image semantics (slow path included, sets `flag`);
 // values_fast(): branch-free, only valid when `bad` stays 0 (FAST kernels).
 
+template <bool LOWP_>
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = 4, CHUNK = 8, MINB = PWB_SYM_LAPLACE_MINB;
-  static constexpr bool FAST = true;
+  static constexpr bool FAST = true, LOWP = LOWP_;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const pwk::LogK& K, int& bad) {
+                                                     const pwk::LogK<LOWP>& K, int& bad) {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -131,10 +132,10 @@ struct SymLaplace {
 template <bool GRAD>
 struct SymModHelm {
   static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0;
-  static constexpr bool FAST = false;
+  static constexpr bool FAST = false, LOWP = false;
   template <int NXI, int NROW>
-  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const pwk::LogK&,
-                                                     int&) {}
+  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&,
+                                                     const pwk::LogK<LOWP>&, int&) {}
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
 #pragma unroll
@@ -190,14 +191,14 @@ struct SymModHelm {
 
 // Stokeslet: V = (log prod r2, Txx, Txy, Tyy [, Px, Py]) with T = sum r r^T / r^2,
 // P = sum r / r^2 (pressurelet, odd).
-template <bool PRESSURE>
+template <bool PRESSURE, bool LOWP_>
 struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
                        CHUNK = 16, MINB = 0;
-  static constexpr bool FAST = true;
+  static constexpr bool FAST = true, LOWP = LOWP_;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const pwk::LogK& K, int& bad) {
+                                                     const pwk::LogK<LOWP>& K, int& bad) {
     double P = 1.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -208,7 +209,7 @@ struct SymStokes {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
-        const double inv = pwk::rcp(r2);
+        const double inv = pwk::rcp_tier<LOWP>(r2);
         const double xi = rx * inv, yi = ry * inv;
         txx = fma(xi, rx, txx);
         txy = fma(xi, ry, txy);
@@ -337,8 +338,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     for (int c = 0; c < K::NACC; ++c) racc[k][c] = 0.0;
   }
   int flag = 0;
-  pwk::LogK LK;
-  if (K::FAST) LK = pwk::log_consts();
+  pwk::LogK<K::LOWP> LK;
+  if (K::FAST) LK = pwk::log_consts<K::LOWP>();
 
   for (int J = J0; J < J1; ++J) {
     const size_t jbase = static_cast<size_t>(J) * TILE;
@@ -559,11 +560,11 @@ long item_count(size_t n) {
 
 long near_sym_item_count(NearKind kind, size_t n) {
   switch (kind) {
-    case NearKind::Laplace: return item_count<SymLaplace>(n);
+    case NearKind::Laplace: return item_count<SymLaplace<false>>(n);
     case NearKind::ModHelm: return item_count<SymModHelm<false>>(n);
     case NearKind::ModHelmGrad: return item_count<SymModHelm<true>>(n);
-    case NearKind::Stokes: return item_count<SymStokes<false>>(n);
-    case NearKind::StokesP: return item_count<SymStokes<true>>(n);
+    case NearKind::Stokes: return item_count<SymStokes<false, false>>(n);
+    case NearKind::StokesP: return item_count<SymStokes<true, false>>(n);
     default: return 0;
   }
 }
@@ -580,11 +581,18 @@ bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned
     return true;
   }
   switch (kind) {
-    case NearKind::Laplace: return dispatch_sym<SymLaplace>(a, st, fx, rsd, rsh, r);
+    // log tier (pw_math.cuh log_pos_k): reduced precision when eps allows it
+    case NearKind::Laplace:
+      return a.lowp_log ? dispatch_sym<SymLaplace<true>>(a, st, fx, rsd, rsh, r)
+                        : dispatch_sym<SymLaplace<false>>(a, st, fx, rsd, rsh, r);
     case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, rsd, rsh, r);
     case NearKind::ModHelmGrad: return dispatch_sym<SymModHelm<true>>(a, st, fx, rsd, rsh, r);
-    case NearKind::Stokes: return dispatch_sym<SymStokes<false>>(a, st, fx, rsd, rsh, r);
-    case NearKind::StokesP: return dispatch_sym<SymStokes<true>>(a, st, fx, rsd, rsh, r);
+    case NearKind::Stokes:
+      return a.lowp_log ? dispatch_sym<SymStokes<false, true>>(a, st, fx, rsd, rsh, r)
+                        : dispatch_sym<SymStokes<false, false>>(a, st, fx, rsd, rsh, r);
+    case NearKind::StokesP:
+      return a.lowp_log ? dispatch_sym<SymStokes<true, true>>(a, st, fx, rsd, rsh, r)
+                        : dispatch_sym<SymStokes<true, false>>(a, st, fx, rsd, rsh, r);
     default: return false;
   }
 }
