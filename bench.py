@@ -255,7 +255,10 @@ def main():
     from paper_2111_01083_b200 import configs
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    # PWB_BENCH_SHARDED=1 runs the multi-GPU code path (NCCL process group, sharded far and
+    # near passes, collectives) even at world size 1, to exercise it on a single-GPU box
+    sharded = ws > 1 or os.environ.get("PWB_BENCH_SHARDED") == "1"
+    if sharded:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -278,7 +281,7 @@ def main():
     str_d = torch.from_numpy(strength).to(dev)
     # targets = sources (c1, c3, c4, c5): hand the library the same array so the symmetric
     # near tile (each unordered pair once) applies; shards and separate targets are copies
-    same = ws == 1 and not c.separate_targets
+    same = not sharded and not c.separate_targets
     tgt_d = src_d if same else torch.from_numpy(np.ascontiguousarray(inp.targets[t_lo:t_hi])).to(dev)
     opt = pw.ApplyOptions(path=pw.ApplyPath.Auto, with_gradient=c.gradient, stream=stream.cuda_stream)
     full = pw.ParticleSystem(sources=src_d, targets=tgt_d, **{kw_name: str_d})
@@ -286,7 +289,7 @@ def main():
     from paper_2111_01083_b200 import dist as pdist
 
     symmetric = not c.separate_targets
-    if ws > 1:
+    if sharded:
         tgt_all = None if symmetric else torch.from_numpy(np.ascontiguousarray(inp.targets)).to(dev)
         backend = pdist.CudaBackend(pw, pz, opt, src_d, str_d, kw_name, tgt_all)
         plan = pdist.ShardPlan(ns, nt, ws, rank)
@@ -294,7 +297,7 @@ def main():
 
     def step():
         nonlocal out
-        if ws == 1:
+        if not sharded:
             out = pw.total_field(pz, full, opt)
             return
         # S2PW on my source slice + allreduce(fp64) of the coefficients; PW2T on my target
@@ -310,7 +313,7 @@ def main():
     launches0 = launch_count(pw)
     near_ms = []
     step_ms = []
-    if ws > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local if ws > 1 else 0) as clocks:
@@ -326,12 +329,12 @@ def main():
             pw.lib().pwb_last_phase_ms(pz.handle, -1, fd, nd)
             near_ms.append(nd._obj.value)
     torch.cuda.synchronize()
-    if ws > 1:
+    if sharded:
         dist.barrier()
     launches = (launch_count(pw) - launches0) / args.steps
     t_step = sum(step_ms) / args.steps
     t_near = sum(near_ms) / args.steps
-    if ws > 1:
+    if sharded:
         tt = torch.tensor([t_step, t_near], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_near = float(tt[0]), float(tt[1])
@@ -344,12 +347,12 @@ def main():
     e2e_ms = []
     host_sys = pw.ParticleSystem(sources=src_h, targets=tgt_h, **{kw_name: str_h})
     for k in range(args.e2e_steps + 1):
-        if ws > 1:
+        if sharded:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if ws == 1:
+        if not sharded:
             r = pw.total_field(pz, host_sys, opt)  # library stages H2D / D2H on `stream`
         else:
             s_d = src_h.to(dev, non_blocking=True)
@@ -363,7 +366,7 @@ def main():
         if k > 0:  # first one warms the staging buffers
             e2e_ms.append(e0.elapsed_time(e1))
     t_e2e = sum(e2e_ms) / len(e2e_ms)
-    if ws > 1:
+    if sharded:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt[0])
@@ -379,7 +382,7 @@ def main():
     pw.lib().pwb_fp64_peak_probe(-1, ctypes.byref(peak))
     nimg = len(pw.near_translations(cell))
     # pairs handled by this rank's near launch (symmetric items split evenly across ranks)
-    pairs = nimg * ns * nt / ws if (symmetric and ws > 1) else nimg * ns * (t_hi - t_lo)
+    pairs = nimg * ns * nt / ws if (symmetric and sharded) else nimg * ns * (t_hi - t_lo)
     flops_near = pairs * F_PAIR[args.config]
     achieved = flops_near / (t_near * 1e-3) / 1e12
     rank_far = pz.rank()
@@ -389,7 +392,7 @@ def main():
     # DFMA instruction peak (peak TFLOP/s / 2)
     pipe_frac = None
     tier = "reduced" if (c.eps >= 1e-11 and not os.environ.get("PWB_FULL_LOG")) else "full"
-    if same and (args.config, tier) in FP64_INSTR_PER_GROUP and ws == 1:
+    if same and (args.config, tier) in FP64_INSTR_PER_GROUP and not sharded:
         groups = ns * (ns + 1) / 2.0
         pipe_frac = groups * FP64_INSTR_PER_GROUP[(args.config, tier)] / (t_near * 1e-3) / (peak.value * 1e12 / 2.0)
 
@@ -411,15 +414,15 @@ def main():
                        "path": "auto", "rank": rank_far, "near_images": nimg,
                        "l2": "256 MB flush buffer written between timed iterations (inputs 24-40 MB < L2)",
                        "parallelism": f"targets split {ws}-way, S2PW sources split {ws}-way + NCCL allreduce"
-                       if ws > 1 else "single GPU"},
+                       if sharded else "single GPU"},
             "e2e": {"value": nt / (t_e2e * 1e-3), "unit": "targets/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                          "frac": achieved / peak.value if peak.value else None,
-                         "traffic": measured_traffic(args.config, ns) if ws == 1 else None,
+                         "traffic": measured_traffic(args.config, ns) if not sharded else None,
                          "log_tier": tier,
-                         "kernel": near_kernel_name(args.config, same and (ns >= 32768 or ws > 1)),
+                         "kernel": near_kernel_name(args.config, same and (ns >= 32768 or sharded)),
                          "near_ms_per_launch": t_near, "far_ms": t_step - t_near,
                          "fp64_pipe_frac": pipe_frac,
                          "note": "frac > 1: the fused symmetric tile evaluates each unordered (target, source)"
@@ -436,7 +439,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
     return 0

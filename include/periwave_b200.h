@@ -159,7 +159,8 @@ typedef struct {
   double nufft_eps;  /* ApplyOptions::nufft_eps (0: derived) */
   int with_gradient; /* extension (scalar kernels): fill pwb_field::gradient */
   int device;        /* CUDA device, -1 = current */
-  void* stream;      /* cudaStream_t, NULL = the library's per-periodizer stream */
+  void* stream;      /* cudaStream_t, NULL = the library's per-periodizer stream (a blocking
+                        stream: ordered after legacy-default-stream work) */
 } pwb_options;
 
 void pwb_options_default(pwb_options* opt);

@@ -155,7 +155,9 @@ __global__ void m0_kernel(const double* mom, int ia, int ib, double a00, double 
 Plan::Plan(const periwave::Periodizer& pz, int device) : pz_(pz), device_(device) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cuda_check(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_), "sm count");
-  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  // A blocking stream: it orders after work the caller queued on the legacy default
+  // stream (e.g. a torch copy of the inputs), so "no stream given" is always safe.
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamDefault), "stream");
   build_families();
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "event");
   flag_.ensure(sizeof(int));

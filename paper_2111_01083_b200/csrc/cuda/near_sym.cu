@@ -37,7 +37,7 @@ namespace pwb {
 namespace {
 
 #ifndef PWB_SYM_LAPLACE_MINB
-#define PWB_SYM_LAPLACE_MINB 5  // 5 x 4 warps/SM (96 regs); 6 (80 regs) spills and measured 1.1 % slower on c4
+#define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
 #endif
 constexpr int kT = 128;  // threads per block
 constexpr int kWarps = kT / 32;
@@ -514,10 +514,18 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
   S.fx = fx;
   S.item0 = static_cast<int>(b);
   if (e > b) {
-    if constexpr (K::MINB > 0)
-      near_sym_kernel_capped<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
-    else
-      near_sym_kernel<K, NXI, NROW><<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
+    // Static shared memory (tile + per-warp column partials) is what limits residency
+    // next to registers: ask for the maximum carveout so registers decide (ncu r1: the
+    // default carveout capped SymLaplace at 5 blocks on shared memory alone).
+    static bool carveout = false;
+    auto* kern = K::MINB > 0 ? near_sym_kernel_capped<K, NXI, NROW> : near_sym_kernel<K, NXI, NROW>;
+    if (!carveout) {
+      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared),
+                 "smem carveout");
+      carveout = true;
+    }
+    kern<<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
     count_launches(1);
   }
   if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, a.out_row, st);
