@@ -244,9 +244,11 @@ int pwb_fast_nufft_available(void);
  * for parity tests. which: 0 bessel_kn(l, x); 1 greens_scalar(pde, beta, r);
  * 2 greens_block (4 out); 3 multipole_kernel(pde, beta, l, r) (2 out);
  * 4 pressurelet (2 out); 5 stresslet_dlp(r, n) (4 out); 6 the symmetric tiles'
- * ln(x) in both precision tiers + the MUFU reciprocal seed + the refined
- * reciprocal of x (4 out, no reference counterpart). Inputs per point:
- * which 0, 6: x (1 double); 1-4: r (2); 5: r, n (4). Host memory. */
+ * ln(x) in both precision tiers, the MUFU reciprocal seed, the refined 1/x,
+ * the MUFU reciprocal-square-root seed and the refined 1/sqrt(x) (6 out, no
+ * reference counterpart); 7 the near tiles' K0(x), K1(x)
+ * in the full and the reduced tier (4 out, x < 64). Inputs per point:
+ * which 0, 6, 7: x (1 double); 1-4: r (2); 5: r, n (4). Host memory. */
 int pwb_eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out);
 
 /* ------------------------------------------------------------ measurement */

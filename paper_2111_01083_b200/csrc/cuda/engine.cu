@@ -836,10 +836,11 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
   a.beta = pz_.beta;
   a.beta2 = pz_.beta * pz_.beta;
   a.xcut2 = 64.0 * 64.0;  // K_0(x) < 3e-29 beyond: below fp64 resolution of any sum
-  // log tier of the symmetric tiles: |error| <= ~3e-13 per pair-log, i.e. >= 1.5 orders
-  // below eps for eps >= 1e-11 (the reference's eps bounds the far truncation); the
-  // full tier is ~1 ulp. PWB_FULL_LOG forces the full tier (tests).
-  a.lowp_log = (pz_.eps >= 1e-11 && std::getenv("PWB_FULL_LOG") == nullptr) ? 1 : 0;
+  // precision tier of the near tiles (pw_math.cuh log_pos_k, k01_tile): the reduced tier
+  // keeps |error| <= ~3e-13 per pair-log and <= 6e-14 relative per Bessel value, >= 1.5
+  // orders below eps for eps >= 1e-11 (the reference's eps bounds the far truncation);
+  // the full tier is ~1 ulp. PWB_FULL_PRECISION forces the full tier (tests).
+  a.lowp = (pz_.eps >= 1e-11 && std::getenv("PWB_FULL_PRECISION") == nullptr) ? 1 : 0;
   if (kind == Kind::Multipole) {
     nk = NearKind::Multipole;
     a.vec = s.coef;

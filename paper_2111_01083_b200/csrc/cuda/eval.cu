@@ -111,15 +111,29 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       out[4 * i + 3] = c * ry * ry;
       break;
     }
-    case 6: {  // the hot tiles' log tiers and reciprocal steps (pw_math.cuh)
+    case 6: {  // the hot tiles' log tiers and reciprocal / rsqrt steps (pw_math.cuh)
       const double x = in[i];
       int bad = 0;
-      out[4 * i] = pwk::log_pos_k<false>(x, pwk::log_consts<false>(), bad);
-      out[4 * i + 1] = pwk::log_pos_k<true>(x, pwk::log_consts<true>(), bad);
-      double r;
+      double* o = out + 6 * i;
+      o[0] = pwk::log_pos_k<false>(x, pwk::log_consts<false>(), bad);
+      o[1] = pwk::log_pos_k<true>(x, pwk::log_consts<true>(), bad);
+      double r, y;
       asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-      out[4 * i + 2] = r;
-      out[4 * i + 3] = pwk::rcp_fast(x);
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+      o[2] = r;
+      o[3] = pwk::rcp_fast(x);
+      o[4] = y;
+      o[5] = pwk::rsqrt(x);
+      break;
+    }
+    case 7: {  // the near tiles' K0 / K1 in both precision tiers (x < 64, pw_math.cuh k01_tile)
+      const double x = in[i];
+      const pwk::K01 f = pwk::k01_tile<false, true>(x * x);
+      const pwk::K01 r = pwk::k01_tile<true, true>(x * x);
+      out[4 * i] = f.k0;
+      out[4 * i + 1] = f.k1_over_x * x;
+      out[4 * i + 2] = r.k0;
+      out[4 * i + 3] = r.k1_over_x * x;
       break;
     }
     default:
@@ -177,8 +191,8 @@ double fp64_peak_probe() {
   return best;
 }
 
-int eval_in_width(int which) { return (which == 0 || which == 6) ? 1 : which == 5 ? 4 : 2; }
-int eval_out_width(int which) { return which <= 1 ? 1 : (which == 3 || which == 4) ? 2 : 4; }
+int eval_in_width(int which) { return (which == 0 || which >= 6) ? 1 : which == 5 ? 4 : 2; }
+int eval_out_width(int which) { return which <= 1 ? 1 : (which == 3 || which == 4) ? 2 : which == 6 ? 6 : 4; }
 
 void run_eval(int which, int pde, double beta, int l, size_t n, const double* in_host, double* out_host) {
   const size_t nin = n * eval_in_width(which), nout = n * eval_out_width(which);

@@ -78,16 +78,17 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
   }
 };
 
+template <bool LOWP>
 struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
   static constexpr int NW = 1, NACC = 1, NOUT = 1;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
                                               const NearArgs& a, int& flag) {
-#pragma unroll
+#pragma unroll 1  // rolled: long Bessel body per image (see near_sym_impl.cuh)
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
-#pragma unroll
+#pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
@@ -98,7 +99,7 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
           }
         }
         const double X = a.beta2 * r2;
-        if (X < a.xcut2) acc[0] = fma(w[0], pwk::k0_of_sq(X), acc[0]);
+        if (X < a.xcut2) acc[0] = fma(w[0], pwk::k01_tile<LOWP, false>(X).k0, acc[0]);
       }
     }
   }
@@ -107,16 +108,17 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
   }
 };
 
+template <bool LOWP>
 struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
   static constexpr int NW = 1, NACC = 3, NOUT = 3;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
                                               const NearArgs& a, int& flag) {
-#pragma unroll
+#pragma unroll 1  // rolled: long Bessel body per image (see near_sym_impl.cuh)
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
-#pragma unroll
+#pragma unroll 1
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
@@ -128,7 +130,7 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
         }
         const double X = a.beta2 * r2;
         if (X < a.xcut2) {
-          const pwk::K01 k = pwk::k01_of_sq(X);
+          const pwk::K01 k = pwk::k01_tile<LOWP, true>(X);
           acc[0] = fma(w[0], k.k0, acc[0]);
           const double g = w[0] * k.k1_over_x;
           acc[1] = fma(g, rx, acc[1]);
@@ -522,8 +524,13 @@ void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* part
   if (a.nt == 0 || a.ns == 0) return;
   switch (kind) {
     case NearKind::Laplace: return dispatch_images<Laplace, 2>(a, st, partial_ws, sm_count);
-    case NearKind::ModHelm: return dispatch_images<ModHelm, 1>(a, st, partial_ws, sm_count);
-    case NearKind::ModHelmGrad: return dispatch_images<ModHelmGrad, 1>(a, st, partial_ws, sm_count);
+    // precision tier (pw_math.cuh k01_tile): reduced when eps allows it
+    case NearKind::ModHelm:
+      return a.lowp ? dispatch_images<ModHelm<true>, 1>(a, st, partial_ws, sm_count)
+                    : dispatch_images<ModHelm<false>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::ModHelmGrad:
+      return a.lowp ? dispatch_images<ModHelmGrad<true>, 1>(a, st, partial_ws, sm_count)
+                    : dispatch_images<ModHelmGrad<false>, 1>(a, st, partial_ws, sm_count);
     case NearKind::Stokes: return dispatch_images<Stokes<false>, 1>(a, st, partial_ws, sm_count);
     case NearKind::StokesP: return dispatch_images<Stokes<true>, 1>(a, st, partial_ws, sm_count);
     case NearKind::ModStokes: return dispatch_images<ModStokes<false>, 1>(a, st, partial_ws, sm_count);

@@ -1,62 +1,11 @@
-// Symmetric near-image P2P for targets == sources (configs c1, c3, c4, c5).
-//
-// The near image set is symmetric (shift <-> -shift, cell.cpp:47-58), so the
-// image-summed kernel of a pair satisfies G3(t_l - s_j) = +/- G3(t_j - s_l)
-// (even part: log, K0, Stokeslet tensor; odd part: gradient, pressurelet). Each
-// unordered pair is evaluated once and feeds both its row (target l, weight w_j)
-// and its column (target j, weight w_l): half the transcendental work of the
-// one-sided tile (near.cu). Exact-zero semantics are unchanged: an exact zero of
-// (t_l - s_j) - shift is an exact zero of (t_j - s_l) + shift (negation is exact),
-// identity-image self pairs are skipped, any other coincidence sets the flag.
-//
-// Work items: row tile I (TILE = 128 * TPT points, TPT per thread) x a chunk of
-// column tiles J >= I (the diagonal tile runs one-sided). Column partials use a
-// rotating schedule (lane l reads column (l + i) mod TILE, one private column
-// copy per warp) so no two lanes of a warp touch the same column and no atomics
-// are needed inside the block.
-//
-// Fast path: for kernels whose per-pair work is a product of image distances
-// (Laplace log, Stokeslet) the off-diagonal tiles run branch-free; a pair whose
-// product is 0 / subnormal / inf (exact coincidence, extreme scales) only raises
-// a flag, and a tile that saw one is redone on the careful per-image path.
-//
-// Row and column sums leave the block through integer atomics on a 3-limb
-// fixed-point accumulator (resolution 2^-62, range 2^64): integer addition is
-// associative, so the result is bitwise deterministic for any schedule, and it
-// is converted back to fp64 once at the end.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-
-#include "near_common.cuh"
-#include "pw_engine.cuh"
-#include "pw_math.cuh"
-#include "pw_pair.cuh"
+// Symmetric near-image P2P for targets == sources: the host-side entry points, the
+// fixed-point readout and the per-kind dispatch. The tile itself (functors, kernel,
+// launcher) is in near_sym_impl.cuh, instantiated per family in near_sym_laplace.cu,
+// near_sym_modhelm.cu and near_sym_stokes.cu.
+#include "near_sym_impl.cuh"
 
 namespace pwb {
 namespace {
-
-#ifndef PWB_SYM_LAPLACE_MINB
-#define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
-#endif
-constexpr int kT = 128;  // threads per block
-constexpr int kWarps = kT / 32;
-
-// ---------------------------------------------------------------- fixed point
-// v = a 2^22 + b 2^-20 + c 2^-62; limbs truncate toward zero so each carries the
-// sign of v and each remainder is exact. Layout: target-major, the three limbs of
-// output c of target l at acc[(l * nout + c) * 3 + {0,1,2}], so a contiguous slice of
-// targets is a contiguous slice of the buffer (the multi-GPU reduce-scatter operand).
-__device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
-  const double a = trunc(v * 0x1p-22);
-  const double r1 = fma(-a, 0x1p22, v);
-  const double b = trunc(r1 * 0x1p20);
-  const double r2 = fma(-b, 0x1p-20, r1);
-  const double c = rint(r2 * 0x1p62);
-  atomicAdd(p, static_cast<unsigned long long>(static_cast<long long>(a)));
-  atomicAdd(p + 1, static_cast<unsigned long long>(static_cast<long long>(b)));
-  atomicAdd(p + 2, static_cast<unsigned long long>(static_cast<long long>(c)));
-}
 
 __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double* out0, int nout0, double* out1,
                                  int nout1, const int* out_row) {
@@ -72,473 +21,6 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
   const int k = static_cast<int>(i % nout);
   double* dst = k < nout0 ? out0 + l * nout0 + k : out1 + l * nout1 + (k - nout0);
   *dst += v;
-}
-
-// ---------------------------------------------------------------- symmetric pair values
-// NV image-summed values per pair; row(acc, V, w_j) and col(acc, V, w_l) contract
-// them with the other side's strength (col flips the odd components).
-// values():      careful per-image semantics (slow path included, sets `flag`);
-// values_fast(): branch-free, only valid when `bad` stays 0 (FAST kernels).
-
-template <bool LOWP_>
-struct SymLaplace {
-  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = 4, CHUNK = 8, MINB = PWB_SYM_LAPLACE_MINB;
-  static constexpr bool FAST = true, LOWP = LOWP_;
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const pwk::LogK<LOWP>& K, int& bad) {
-    double ry2[NROW];
-#pragma unroll
-    for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
-      ry2[n] = ry * ry;
-    }
-    double P = 1.0;
-#pragma unroll
-    for (int n = 0; n < NROW; ++n)
-#pragma unroll
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        P *= fma(rx, rx, ry2[n]);
-      }
-    V[0] = pwk::log_pos_k(P, K, bad);
-  }
-  template <int NXI, int NROW>
-  __device__ __noinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
-    double L = 0.0;
-    for (int n = 0; n < NROW; ++n)
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = row_dy<NXI, NROW>(dy, a, n);
-        if (rx == 0.0 && ry == 0.0) {
-          if (n * NXI + m != a.id_img) flag = 1;
-          continue;
-        }
-        L += pwk::log_r2_safe(rx, ry);
-      }
-    V[0] = L;
-  }
-  __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
-    acc[0] = fma(w[0], V[0], acc[0]);
-  }
-  __device__ __forceinline__ static void col(double* acc, const double* V, const double* w) {
-    acc[0] = fma(w[0], V[0], acc[0]);
-  }
-  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
-    out[0] = acc[0] * (-1.0 / (4.0 * pwk::kPi));
-  }
-};
-
-template <bool GRAD>
-struct SymModHelm {
-  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0;
-  static constexpr bool FAST = false, LOWP = false;
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&,
-                                                     const pwk::LogK<LOWP>&, int&) {}
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) V[v] = 0.0;
-#pragma unroll
-    for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
-      const double ry2 = ry * ry;
-#pragma unroll
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double r2 = fma(rx, rx, ry2);
-        if (r2 == 0.0) {
-          if (rx == 0.0 && ry == 0.0) {
-            if (n * NXI + m != a.id_img) flag = 1;
-            continue;
-          }
-        }
-        const double X = a.beta2 * r2;
-        if (X < a.xcut2) {
-          if (GRAD) {
-            const pwk::K01 k = pwk::k01_of_sq(X);
-            V[0] += k.k0;
-            V[1] = fma(k.k1_over_x, rx, V[1]);
-            V[2] = fma(k.k1_over_x, ry, V[2]);
-          } else {
-            V[0] += pwk::k0_of_sq(X);
-          }
-        }
-      }
-    }
-  }
-  __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc[v] = fma(w[0], V[v], acc[v]);
-  }
-  __device__ __forceinline__ static void col(double* acc, const double* V, const double* w) {
-    acc[0] = fma(w[0], V[0], acc[0]);
-    if (GRAD) {  // the gradient kernel is odd in r
-      acc[1] = fma(-w[0], V[1], acc[1]);
-      acc[2] = fma(-w[0], V[2], acc[2]);
-    }
-  }
-  __device__ __forceinline__ static void finish(const double* acc, const NearArgs& a, double* out) {
-    out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
-    if (GRAD) {
-      const double gs = -a.beta2 / (2.0 * pwk::kPi);
-      out[1] = acc[1] * gs;
-      out[2] = acc[2] * gs;
-    }
-  }
-};
-
-// Stokeslet: V = (log prod r2, Txx, Txy, Tyy [, Px, Py]) with T = sum r r^T / r^2,
-// P = sum r / r^2 (pressurelet, odd).
-template <bool PRESSURE, bool LOWP_>
-struct SymStokes {
-  static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
-                       CHUNK = 16, MINB = 0;
-  static constexpr bool FAST = true, LOWP = LOWP_;
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const pwk::LogK<LOWP>& K, int& bad) {
-    double P = 1.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
-#pragma unroll
-    for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
-      const double ry2 = ry * ry;
-#pragma unroll
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double r2 = fma(rx, rx, ry2);
-        P *= r2;
-        const double inv = pwk::rcp_tier<LOWP>(r2);
-        const double xi = rx * inv, yi = ry * inv;
-        txx = fma(xi, rx, txx);
-        txy = fma(xi, ry, txy);
-        tyy = fma(yi, ry, tyy);
-        if (PRESSURE) {
-          px += xi;
-          py += yi;
-        }
-      }
-    }
-    V[0] = pwk::log_pos_k(P, K, bad);
-    V[1] = txx;
-    V[2] = txy;
-    V[3] = tyy;
-    if (PRESSURE) {
-      V[4] = px;
-      V[5] = py;
-    }
-  }
-  template <int NXI, int NROW>
-  __device__ __noinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
-    double L = 0.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
-    for (int n = 0; n < NROW; ++n)
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = row_dy<NXI, NROW>(dy, a, n);
-        if (rx == 0.0 && ry == 0.0) {
-          if (n * NXI + m != a.id_img) flag = 1;
-          continue;
-        }
-        const double r2 = fma(rx, rx, ry * ry);
-        L += pwk::log_r2_safe(rx, ry);
-        txx += rx * rx / r2;
-        txy += rx * ry / r2;
-        tyy += ry * ry / r2;
-        px += rx / r2;
-        py += ry / r2;
-      }
-    V[0] = L;
-    V[1] = txx;
-    V[2] = txy;
-    V[3] = tyy;
-    if (PRESSURE) {
-      V[4] = px;
-      V[5] = py;
-    }
-  }
-  // acc = (L fx, L fy, (T f)_x, (T f)_y [, P.f])
-  __device__ __forceinline__ static void contract(double* acc, const double* V, const double* w, double sgn) {
-    acc[0] = fma(V[0], w[0], acc[0]);
-    acc[1] = fma(V[0], w[1], acc[1]);
-    acc[2] = fma(V[1], w[0], fma(V[2], w[1], acc[2]));
-    acc[3] = fma(V[2], w[0], fma(V[3], w[1], acc[3]));
-    if (PRESSURE) acc[4] = fma(sgn * V[4], w[0], fma(sgn * V[5], w[1], acc[4]));
-  }
-  __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
-    contract(acc, V, w, 1.0);
-  }
-  __device__ __forceinline__ static void col(double* acc, const double* V, const double* w) {
-    contract(acc, V, w, -1.0);
-  }
-  __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
-    const double c = -1.0 / (4.0 * pwk::kPi);
-    out[0] = c * fma(0.5, acc[0], -acc[2]);
-    out[1] = c * fma(0.5, acc[1], -acc[3]);
-    if (PRESSURE) out[2] = acc[4] * (1.0 / (2.0 * pwk::kPi));
-  }
-};
-
-// ---------------------------------------------------------------- the kernel
-struct SymArgs {
-  NearArgs a;
-  int nb;                  // number of TILE-point tiles
-  int chunk;               // column tiles per work item
-  const int* row_start;    // [nb + 1] first work item of each row tile
-  unsigned long long* fx;  // fixed-point accumulators [n][nout][3]
-  int item0;               // first work item of this launch (multi-GPU item ranges)
-};
-
-template <class K>
-__device__ __forceinline__ void load_w(const NearArgs& a, size_t j, bool live, double* w) {
-  if (K::NW == 1) {
-    w[0] = live ? a.q[j] : 0.0;
-  } else {
-    const double2 v = live ? a.vec[j] : make_double2(0.0, 0.0);
-    w[0] = v.x;
-    w[K::NW > 1 ? 1 : 0] = v.y;
-  }
-}
-
-template <class K, int NXI, int NROW>
-__device__ __forceinline__ void near_sym_body(const SymArgs& S) {
-  constexpr int TPT = K::TPT;
-  constexpr int TILE = kT * TPT;
-  const NearArgs& a = S.a;
-  __shared__ double s_x[TILE], s_y[TILE], s_w[K::NW][TILE];
-  __shared__ double s_col[kWarps][K::NACC][TILE];
-
-  // work item -> (row tile I, first column tile)
-  const int item = S.item0 + static_cast<int>(blockIdx.x);
-  int lo = 0, hi = S.nb;  // row_start[I] <= item < row_start[I+1]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (S.row_start[mid] <= item)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  const int I = lo;
-  const int J0 = I + (item - S.row_start[I]) * S.chunk;
-  const int J1 = min(S.nb, J0 + S.chunk);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t n = a.nt;
-  double tx[TPT], ty[TPT], tw[TPT][K::NW], racc[TPT][K::NACC];
-  bool live[TPT];
-#pragma unroll
-  for (int k = 0; k < TPT; ++k) {
-    const size_t l = static_cast<size_t>(I) * TILE + tid + k * kT;
-    live[k] = l < n;
-    const double2 p = live[k] ? a.tgt[l] : make_double2(0.0, 0.0);  // dead: origin, weight 0
-    tx[k] = p.x;
-    ty[k] = p.y;
-    load_w<K>(a, l, live[k], tw[k]);
-#pragma unroll
-    for (int c = 0; c < K::NACC; ++c) racc[k][c] = 0.0;
-  }
-  int flag = 0;
-  pwk::LogK<K::LOWP> LK;
-  if (K::FAST) LK = pwk::log_consts<K::LOWP>();
-
-  for (int J = J0; J < J1; ++J) {
-    const size_t jbase = static_cast<size_t>(J) * TILE;
-    __syncthreads();
-    for (int i = tid; i < TILE; i += kT) {
-      const size_t j = jbase + i;
-      const bool lv = j < n;
-      const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);
-      s_x[i] = p.x;
-      s_y[i] = p.y;
-      double w[K::NW];
-      load_w<K>(a, j, lv, w);
-#pragma unroll
-      for (int c = 0; c < K::NW; ++c) s_w[c][i] = w[c];
-#pragma unroll
-      for (int c = 0; c < K::NACC; ++c)
-#pragma unroll
-        for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
-    }
-    __syncthreads();
-    if (J == I) {  // diagonal tile: one-sided and careful (self pairs live here)
-      for (int i = 0; i < TILE; ++i) {
-        const double sx = s_x[i], sy = s_y[i];
-        double w[K::NW];
-#pragma unroll
-        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][i];
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          double V[K::NV];
-          K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
-          K::row(racc[k], V, w);
-        }
-      }
-      continue;
-    }
-    bool careful = !K::FAST;
-    if (K::FAST) {
-      double keep[TPT][K::NACC];
-#pragma unroll
-      for (int k = 0; k < TPT; ++k)
-#pragma unroll
-        for (int c = 0; c < K::NACC; ++c) keep[k][c] = racc[k][c];
-      int bad = 0;
-#pragma unroll 2
-      for (int i = 0; i < TILE; ++i) {
-        const int jj = (lane + i) & (TILE - 1);
-        const double sx = s_x[jj], sy = s_y[jj];
-        double w[K::NW];
-#pragma unroll
-        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
-        double cacc[K::NACC];
-#pragma unroll
-        for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          double V[K::NV];
-          // (t - s) - shift as upstream (apply.cpp:534)
-          K::template values_fast<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
-          K::row(racc[k], V, w);
-          K::col(cacc, V, tw[k]);
-        }
-#pragma unroll
-        for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
-      }
-      if (__syncthreads_or(bad)) {  // rare: redo this tile on the careful path
-#pragma unroll
-        for (int k = 0; k < TPT; ++k)
-#pragma unroll
-          for (int c = 0; c < K::NACC; ++c) racc[k][c] = keep[k][c];
-        for (int i = tid; i < TILE; i += kT)
-#pragma unroll
-          for (int c = 0; c < K::NACC; ++c)
-#pragma unroll
-            for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
-        __syncthreads();
-        careful = true;
-      }
-    }
-    if (careful) {
-#pragma unroll 1
-      for (int i = 0; i < TILE; ++i) {
-        const int jj = (lane + i) & (TILE - 1);
-        const double sx = s_x[jj], sy = s_y[jj];
-        double w[K::NW];
-#pragma unroll
-        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
-        double cacc[K::NACC];
-#pragma unroll
-        for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          double V[K::NV];
-          K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
-          K::row(racc[k], V, w);
-          K::col(cacc, V, tw[k]);
-        }
-#pragma unroll
-        for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
-      }
-    }
-    __syncthreads();
-    // column totals of this tile -> fixed point
-    for (int i = tid; i < TILE; i += kT) {
-      const size_t j = jbase + i;
-      if (j >= n) continue;
-      double acc[K::NACC];
-#pragma unroll
-      for (int c = 0; c < K::NACC; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int wv = 0; wv < kWarps; ++wv) s += s_col[wv][c][i];
-        acc[c] = s;
-      }
-      double o[K::NOUT];
-      K::finish(acc, a, o);
-#pragma unroll
-      for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (j * K::NOUT + c) * 3, o[c]);
-    }
-  }
-  if (flag) atomicOr(a.flag, 1);
-#pragma unroll
-  for (int k = 0; k < TPT; ++k) {
-    if (!live[k]) continue;
-    const size_t l = static_cast<size_t>(I) * TILE + tid + k * kT;
-    double o[K::NOUT];
-    K::finish(racc[k], a, o);
-#pragma unroll
-    for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (l * K::NOUT + c) * 3, o[c]);
-  }
-}
-
-
-// K::MINB > 0 caps registers for K::MINB resident blocks per SM (one image row; the 2-D
-// image blocks hold more live shifts and get at most 4 -- 80 or 96 regs spill there).
-// MINB == 0 keeps ptxas's own allocation (the wider functors).
-template <class K, int NXI, int NROW>
-__global__ void __launch_bounds__(kT, NROW == 1 ? K::MINB : (K::MINB < 4 ? K::MINB : 4))
-    near_sym_kernel_capped(const __grid_constant__ SymArgs S) {
-  near_sym_body<K, NXI, NROW>(S);
-}
-
-template <class K, int NXI, int NROW>
-__global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
-  near_sym_body<K, NXI, NROW>(S);
-}
-
-template <class K, int NXI, int NROW>
-void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                      int* row_start_host, const SymRange& range) {
-  constexpr int TILE = kT * K::TPT;
-  const int chunk = K::CHUNK;
-  const int nb = static_cast<int>((a.nt + TILE - 1) / TILE);
-  int items = 0;
-  for (int I = 0; I < nb; ++I) {
-    row_start_host[I] = items;
-    items += (nb - I + chunk - 1) / chunk;
-  }
-  row_start_host[nb] = items;
-  if (range.total_items) *range.total_items = items;
-  if (range.count_only) return;
-  const long b = range.begin < 0 ? 0 : std::min<long>(range.begin, items);
-  const long e = range.end < 0 ? items : std::min<long>(range.end, items);
-  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
-             "row starts");
-  const size_t nout = K::NOUT;
-  if (range.finish) cuda_check(cudaMemsetAsync(fx, 0, 3 * a.nt * nout * sizeof(unsigned long long), st), "memset fx");
-  SymArgs S;
-  S.a = a;
-  S.nb = nb;
-  S.chunk = chunk;
-  S.row_start = row_start_dev;
-  S.fx = fx;
-  S.item0 = static_cast<int>(b);
-  if (e > b) {
-    // Static shared memory (tile + per-warp column partials) is what limits residency
-    // next to registers: ask for the maximum carveout so registers decide (ncu r1: the
-    // default carveout capped SymLaplace at 5 blocks on shared memory alone).
-    static bool carveout = false;
-    auto* kern = K::MINB > 0 ? near_sym_kernel_capped<K, NXI, NROW> : near_sym_kernel<K, NXI, NROW>;
-    if (!carveout) {
-      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      cudaSharedmemCarveoutMaxShared),
-                 "smem carveout");
-      carveout = true;
-    }
-    kern<<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
-    count_launches(1);
-  }
-  if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, a.out_row, st);
-}
-
-template <class K>
-bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
-                  const SymRange& r) {
-  if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh, r), true;
-  if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh, r), true;
-  if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh, r), true;
-  if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh, r), true;
-  return false;
 }
 
 }  // namespace
@@ -558,7 +40,7 @@ size_t near_sym_tiles(size_t n) { return (n + 255) / 256; }
 namespace {
 template <class K>
 long item_count(size_t n) {
-  const size_t tile = static_cast<size_t>(kT) * K::TPT;
+  const size_t tile = static_cast<size_t>(sym::kT) * K::TPT;
   const long nb = static_cast<long>((n + tile - 1) / tile);
   long items = 0;
   for (long I = 0; I < nb; ++I) items += (nb - I + K::CHUNK - 1) / K::CHUNK;
@@ -568,11 +50,11 @@ long item_count(size_t n) {
 
 long near_sym_item_count(NearKind kind, size_t n) {
   switch (kind) {
-    case NearKind::Laplace: return item_count<SymLaplace<false>>(n);
-    case NearKind::ModHelm: return item_count<SymModHelm<false>>(n);
-    case NearKind::ModHelmGrad: return item_count<SymModHelm<true>>(n);
-    case NearKind::Stokes: return item_count<SymStokes<false, false>>(n);
-    case NearKind::StokesP: return item_count<SymStokes<true, false>>(n);
+    case NearKind::Laplace: return item_count<sym::SymLaplace<false>>(n);
+    case NearKind::ModHelm: return item_count<sym::SymModHelm<false, false>>(n);
+    case NearKind::ModHelmGrad: return item_count<sym::SymModHelm<true, false>>(n);
+    case NearKind::Stokes: return item_count<sym::SymStokes<false, false>>(n);
+    case NearKind::StokesP: return item_count<sym::SymStokes<true, false>>(n);
     default: return 0;
   }
 }
@@ -588,19 +70,13 @@ bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned
     if (r.total_items) *r.total_items = 0;
     return true;
   }
+  // precision tier (pw_math.cuh log_pos_k / k01_tile): reduced when eps allows it
   switch (kind) {
-    // log tier (pw_math.cuh log_pos_k): reduced precision when eps allows it
-    case NearKind::Laplace:
-      return a.lowp_log ? dispatch_sym<SymLaplace<true>>(a, st, fx, rsd, rsh, r)
-                        : dispatch_sym<SymLaplace<false>>(a, st, fx, rsd, rsh, r);
-    case NearKind::ModHelm: return dispatch_sym<SymModHelm<false>>(a, st, fx, rsd, rsh, r);
-    case NearKind::ModHelmGrad: return dispatch_sym<SymModHelm<true>>(a, st, fx, rsd, rsh, r);
+    case NearKind::Laplace: return sym::launch_laplace(a, st, fx, rsd, rsh, r);
+    case NearKind::ModHelm:
+    case NearKind::ModHelmGrad: return sym::launch_modhelm(kind, a, st, fx, rsd, rsh, r);
     case NearKind::Stokes:
-      return a.lowp_log ? dispatch_sym<SymStokes<false, true>>(a, st, fx, rsd, rsh, r)
-                        : dispatch_sym<SymStokes<false, false>>(a, st, fx, rsd, rsh, r);
-    case NearKind::StokesP:
-      return a.lowp_log ? dispatch_sym<SymStokes<true, true>>(a, st, fx, rsd, rsh, r)
-                        : dispatch_sym<SymStokes<true, false>>(a, st, fx, rsd, rsh, r);
+    case NearKind::StokesP: return sym::launch_stokes(kind, a, st, fx, rsd, rsh, r);
     default: return false;
   }
 }

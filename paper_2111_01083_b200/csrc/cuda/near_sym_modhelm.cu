@@ -1,0 +1,17 @@
+// Instantiations of the symmetric near tile: modified-Helmholtz tiles (SymModHelm, with / without gradient, both tiers).
+#include "near_sym_impl.cuh"
+
+namespace pwb {
+namespace sym {
+
+bool launch_modhelm(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd,
+                    int* rsh, const SymRange& r) {
+  if (kind == NearKind::ModHelmGrad)
+    return a.lowp ? dispatch_sym<SymModHelm<true, true>>(a, st, fx, rsd, rsh, r)
+                  : dispatch_sym<SymModHelm<true, false>>(a, st, fx, rsd, rsh, r);
+  return a.lowp ? dispatch_sym<SymModHelm<false, true>>(a, st, fx, rsd, rsh, r)
+                : dispatch_sym<SymModHelm<false, false>>(a, st, fx, rsd, rsh, r);
+}
+
+}  // namespace sym
+}  // namespace pwb

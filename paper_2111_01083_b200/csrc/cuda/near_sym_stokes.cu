@@ -1,0 +1,17 @@
+// Instantiations of the symmetric near tile: Stokeslet tiles (SymStokes, with / without pressure, both tiers).
+#include "near_sym_impl.cuh"
+
+namespace pwb {
+namespace sym {
+
+bool launch_stokes(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd,
+                   int* rsh, const SymRange& r) {
+  if (kind == NearKind::StokesP)
+    return a.lowp ? dispatch_sym<SymStokes<true, true>>(a, st, fx, rsd, rsh, r)
+                  : dispatch_sym<SymStokes<true, false>>(a, st, fx, rsd, rsh, r);
+  return a.lowp ? dispatch_sym<SymStokes<false, true>>(a, st, fx, rsd, rsh, r)
+                : dispatch_sym<SymStokes<false, false>>(a, st, fx, rsd, rsh, r);
+}
+
+}  // namespace sym
+}  // namespace pwb

@@ -51,7 +51,7 @@ struct NearArgs {
   size_t src_per_split = 0;
   int* flag = nullptr;     // set to 1 on a non-identity exact coincidence
   const int* out_row = nullptr;  // binned targets: output row of target l (nullptr: l)
-  int lowp_log = 0;              // symmetric tiles: reduced-precision log tier (eps >= 1e-11)
+  int lowp = 0;                  // near tiles: reduced-precision tier (eps >= 1e-11, pw_math.cuh)
 };
 
 // ---------------------------------------------------------------- spatial binning (binning.cu)

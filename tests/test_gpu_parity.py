@@ -418,3 +418,22 @@ def test_hot_tile_log_and_reciprocal_tiers(pw, gpu):
     y = rng.uniform(1e-3, 1e3, 20000)
     r = pw.eval_kernel(6, 0, 0.0, 0, y)
     assert np.max(np.abs(r[:, 3] * y - 1.0)) <= 4e-16
+    # MUFU reciprocal-square-root seed (sets how many Newton steps the Bessel tiles need)
+    rs_seed = np.abs(r[:, 4] * np.sqrt(y) - 1.0).max()
+    print("rsqrt seed max rel error", rs_seed, "rcp seed", np.abs(r[:, 2] * y - 1.0).max())
+    assert rs_seed <= 2.0 ** -12
+    assert np.max(np.abs(r[:, 5] * np.sqrt(y) - 1.0)) <= 4e-16
+
+
+def test_hot_tile_bessel_tiers(pw, gpu, ref):
+    """The near tiles' K0 / K1 (pw_math.cuh k01_tile: series, split asymptotics) in both
+    precision tiers against the reference's Bessel functions, over the tiles' range x < 64."""
+    xs = np.concatenate([np.geomspace(1e-6, 1.999, 200), [2.0, 2.0000001, 5.999999, 6.0, 6.0000001],
+                         np.geomspace(2.0001, 63.99, 400)])
+    out = pw.eval_kernel(7, 0, 0.0, 0, xs)
+    for l, cf, cl in ((0, 0, 2), (1, 1, 3)):
+        want = np.array([ref.bessel_kn(l, x) for x in xs])
+        full = np.abs(out[:, cf] - want) / want
+        low = np.abs(out[:, cl] - want) / want
+        assert np.all(full <= 4e-15 + 3e-16 * xs), (l, xs[np.argmax(full)], full.max())
+        assert np.all(low <= 2e-13 + 3e-16 * xs), (l, xs[np.argmax(low)], low.max())
