@@ -43,6 +43,12 @@ namespace pwb {
 namespace sym {
 
 
+#ifndef PWB_SYM_LAPLACE_TPT
+#define PWB_SYM_LAPLACE_TPT 4  // targets per thread of the Laplace tile
+#endif
+#ifndef PWB_SYM_LAPLACE_UNROLL
+#define PWB_SYM_LAPLACE_UNROLL 4  // sources per unrolled step of the fast loop (c4: 904 -> 895 ms vs 2)
+#endif
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
 #endif
@@ -73,7 +79,8 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
 
 template <bool LOWP_>
 struct SymLaplace {
-  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = 4, CHUNK = 8, MINB = PWB_SYM_LAPLACE_MINB;
+  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT, CHUNK = 8,
+                       MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -122,7 +129,7 @@ struct SymLaplace {
 
 template <bool GRAD, bool LOWP_>
 struct SymModHelm {
-  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0;
+  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0, UNROLL = 1;
   static constexpr bool FAST = false, LOWP = LOWP_;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&,
@@ -185,12 +192,12 @@ struct SymModHelm {
 template <bool PRESSURE, bool LOWP_>
 struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
-                       CHUNK = 16, MINB = 0;
+                       CHUNK = 16, MINB = 0, UNROLL = 2;
   static constexpr bool FAST = true, LOWP = LOWP_;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const pwk::LogK<LOWP>& K, int& bad) {
-    double P = 1.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
+    double P = 1.0, txx = 0.0, txy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
@@ -201,20 +208,21 @@ struct SymStokes {
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
         const double inv = pwk::rcp_tier<LOWP>(r2);
-        const double xi = rx * inv, yi = ry * inv;
+        const double xi = rx * inv;
         txx = fma(xi, rx, txx);
         txy = fma(xi, ry, txy);
-        tyy = fma(yi, ry, tyy);
         if (PRESSURE) {
           px += xi;
-          py += yi;
+          py = fma(ry, inv, py);
         }
       }
     }
     V[0] = pwk::log_pos_k(P, K, bad);
     V[1] = txx;
     V[2] = txy;
-    V[3] = tyy;
+    // rx^2/r^2 + ry^2/r^2 = 1 per image (no exact zero on this path): trace = image count,
+    // to ~2 ulp per image -- one DADD instead of an fma and a multiply per image
+    V[3] = static_cast<double>(NXI * NROW) - txx;
     if (PRESSURE) {
       V[4] = px;
       V[5] = py;
@@ -374,7 +382,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int c = 0; c < K::NACC; ++c) keep[k][c] = racc[k][c];
       int bad = 0;
-#pragma unroll 2
+#pragma unroll K::UNROLL
       for (int i = 0; i < TILE; ++i) {
         const int jj = (lane + i) & (TILE - 1);
         const double sx = s_x[jj], sy = s_y[jj];
@@ -509,7 +517,11 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
     // next to registers: ask for the maximum carveout so registers decide (ncu r1: the
     // default carveout capped SymLaplace at 5 blocks on shared memory alone).
     static bool carveout = false;
-    auto* kern = K::MINB > 0 ? near_sym_kernel_capped<K, NXI, NROW> : near_sym_kernel<K, NXI, NROW>;
+    void (*kern)(const SymArgs);
+    if constexpr (K::MINB > 0)
+      kern = near_sym_kernel_capped<K, NXI, NROW>;
+    else
+      kern = near_sym_kernel<K, NXI, NROW>;
     if (!carveout) {
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       cudaSharedmemCarveoutMaxShared),
