@@ -437,3 +437,42 @@ def test_hot_tile_bessel_tiers(pw, gpu, ref):
         low = np.abs(out[:, cl] - want) / want
         assert np.all(full <= 4e-15 + 3e-16 * xs), (l, xs[np.argmax(full)], full.max())
         assert np.all(low <= 2e-13 + 3e-16 * xs), (l, xs[np.argmax(low)], low.max())
+
+
+@pytest.mark.parametrize("pde,beta,strength", [("Poisson", 0.0, "charge"), ("ModHelmholtz", 2.0, "charge"),
+                                               ("Stokes", 0.0, "force")])
+def test_symmetric_tile_duplicates_and_image_coincidence(pw, gpu, pde, beta, strength):
+    """Above the symmetric threshold: duplicate points (exact zeros in the identity image,
+    skipped like the reference's self pairs, test_apply.cpp:181-218) take the careful
+    path and agree with the one-sided tile; a point on the cell face that coincides with
+    a near image of another point raises CoincidentSourceTarget on both paths."""
+    rng = np.random.default_rng(99)
+    n = 33000
+    src = rng.uniform(-0.45, 0.45, (n, 2))
+    src[1000:1010] = src[20000:20010]  # duplicates across different tiles
+    src[5] = src[6]                     # and inside one tile
+    if strength == "charge":
+        w = rng.uniform(-1, 1, n)
+        if pde == "Poisson":
+            w -= w.mean()
+        kw = dict(charges=np.ascontiguousarray(w))
+    else:
+        f = rng.uniform(-1, 1, (n, 2))
+        kw = dict(forces=np.ascontiguousarray(f - f.mean(axis=0)))
+    cell = pw.make_unit_cell(1.0, 0.0, 1.0)
+    pz = pw.make_periodizer(pw.Pde[pde], beta, cell, 1e-10)
+    src = np.ascontiguousarray(src)
+    key = "scalar" if strength == "charge" else "velocity"
+    sym = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw)), key)
+    one = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), **kw)), key)
+    assert np.all(np.isfinite(sym))
+    assert rel_l2(sym, one) <= 1e-12
+    bad = src.copy()
+    bad[7] = [0.3, -0.5]
+    bad[30000] = [0.3, 0.5]  # the (0, +1) image of point 7
+    with pytest.raises(pw.PeriwaveError) as e:
+        pw.near_field(pz, pw.ParticleSystem(sources=bad, targets=bad, **kw))
+    assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
+    with pytest.raises(pw.PeriwaveError) as e:
+        pw.near_field(pz, pw.ParticleSystem(sources=bad, targets=bad.copy(), **kw))
+    assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
