@@ -24,6 +24,18 @@
 #include "pw_pair.cuh"
 #include "near_common.cuh"
 
+#ifndef PWB_MH_UNROLL_M
+#define PWB_MH_UNROLL_M 3  // image columns per unrolled step (screened kernels; c2: 1 -> 929 ms, 2 -> 807, 3 -> 792, 5 -> 890)
+#endif
+#ifndef PWB_MH_TPT
+#define PWB_MH_TPT 1  // targets per thread of the screened one-sided tiles
+#endif
+namespace pwb {
+namespace {
+constexpr int kMhUnrollM = PWB_MH_UNROLL_M;
+}
+}  // namespace pwb
+
 namespace pwb {
 namespace {
 
@@ -84,11 +96,11 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
                                               const NearArgs& a, int& flag) {
-#pragma unroll 1  // rolled: long Bessel body per image (see near_sym_impl.cuh)
+#pragma unroll 1  // rows rolled: long Bessel body per image (see near_sym_impl.cuh)
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
-#pragma unroll 1
+#pragma unroll kMhUnrollM
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
@@ -114,11 +126,11 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
                                               const NearArgs& a, int& flag) {
-#pragma unroll 1  // rolled: long Bessel body per image (see near_sym_impl.cuh)
+#pragma unroll 1  // rows rolled: long Bessel body per image (see near_sym_impl.cuh)
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
-#pragma unroll 1
+#pragma unroll kMhUnrollM
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
@@ -526,11 +538,11 @@ void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* part
     case NearKind::Laplace: return dispatch_images<Laplace, 2>(a, st, partial_ws, sm_count);
     // precision tier (pw_math.cuh k01_tile): reduced when eps allows it
     case NearKind::ModHelm:
-      return a.lowp ? dispatch_images<ModHelm<true>, 1>(a, st, partial_ws, sm_count)
-                    : dispatch_images<ModHelm<false>, 1>(a, st, partial_ws, sm_count);
+      return a.lowp ? dispatch_images<ModHelm<true>, PWB_MH_TPT>(a, st, partial_ws, sm_count)
+                    : dispatch_images<ModHelm<false>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
     case NearKind::ModHelmGrad:
-      return a.lowp ? dispatch_images<ModHelmGrad<true>, 1>(a, st, partial_ws, sm_count)
-                    : dispatch_images<ModHelmGrad<false>, 1>(a, st, partial_ws, sm_count);
+      return a.lowp ? dispatch_images<ModHelmGrad<true>, PWB_MH_TPT>(a, st, partial_ws, sm_count)
+                    : dispatch_images<ModHelmGrad<false>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
     case NearKind::Stokes: return dispatch_images<Stokes<false>, 1>(a, st, partial_ws, sm_count);
     case NearKind::StokesP: return dispatch_images<Stokes<true>, 1>(a, st, partial_ws, sm_count);
     case NearKind::ModStokes: return dispatch_images<ModStokes<false>, 1>(a, st, partial_ws, sm_count);

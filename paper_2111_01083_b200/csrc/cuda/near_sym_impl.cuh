@@ -46,6 +46,9 @@ namespace sym {
 #ifndef PWB_SYM_LAPLACE_TPT
 #define PWB_SYM_LAPLACE_TPT 4  // targets per thread of the Laplace tile
 #endif
+#ifndef PWB_SYM_MH_UNROLL_M
+#define PWB_SYM_MH_UNROLL_M 3  // image columns per unrolled step of the screened symmetric tile (c5 slice: 1 -> 573 ms, 3 -> 480)
+#endif
 #ifndef PWB_SYM_LAPLACE_UNROLL
 #define PWB_SYM_LAPLACE_UNROLL 4  // sources per unrolled step of the fast loop (c4: 904 -> 895 ms vs 2)
 #endif
@@ -53,6 +56,7 @@ namespace sym {
 #define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
 #endif
 constexpr int kT = 128;  // threads per block
+constexpr int kSymMhUnrollM = PWB_SYM_MH_UNROLL_M;
 constexpr int kWarps = kT / 32;
 
 // ---------------------------------------------------------------- fixed point
@@ -144,7 +148,7 @@ struct SymModHelm {
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
-#pragma unroll 1
+#pragma unroll kSymMhUnrollM
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
