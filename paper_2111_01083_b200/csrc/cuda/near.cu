@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "pw_engine.cuh"
 #include "pw_math.cuh"
@@ -47,11 +48,14 @@ constexpr int kTile = 256;
 // NOUT output doubles per target, pair<NXI,NROW>(acc, dx, dy, w, args, flag),
 // finish(acc, args, out[NOUT]).
 
+template <bool LOWP>
 struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
   static constexpr int NW = 1, NACC = 1, NOUT = 1;
+  using Consts = pwk::LogK<LOWP>;  // register-resident log constants (pw_math.cuh)
+  __device__ __forceinline__ static Consts consts() { return pwk::log_consts<LOWP>(); }
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
-                                              const NearArgs& a, int& flag) {
+                                              const NearArgs& a, int& flag, const Consts& C) {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -66,8 +70,10 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         P *= fma(rx, rx, ry2[n]);
       }
-    if (normal_pos(P)) {
-      acc[0] = fma(w[0], pwk::log_pos(P), acc[0]);
+    int bad = 0;
+    const double LP = pwk::log_pos_k<LOWP>(P, C, bad);
+    if (!bad) {
+      acc[0] = fma(w[0], LP, acc[0]);
       return;
     }
     double L = 0.0;
@@ -161,12 +167,14 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
 
 // Stokeslet -(1/4pi)(log|r| I - r r^T/|r|^2) f  (kernels.cpp:115-119), plus the
 // optional pressurelet r.f/(2 pi r^2) (kernels.cpp:139-143).
-template <bool PRESSURE>
+template <bool PRESSURE, bool LOWP>
 struct Stokes {
   static constexpr int NW = 2, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2;
+  using Consts = pwk::LogK<LOWP>;
+  __device__ __forceinline__ static Consts consts() { return pwk::log_consts<LOWP>(); }
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
-                                              const NearArgs& a, int& flag) {
+                                              const NearArgs& a, int& flag, const Consts& C) {
     double P = 1.0;
     double ax = 0.0, ay = 0.0, pr = 0.0;
 #pragma unroll
@@ -179,14 +187,15 @@ struct Stokes {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
-        const double t = fma(w[0], rx, fy_ry) * pwk::rcp(r2);
+        const double t = fma(w[0], rx, fy_ry) * pwk::rcp_tier<LOWP>(r2);
         ax = fma(rx, t, ax);
         ay = fma(ry, t, ay);
         if (PRESSURE) pr += t;
       }
     }
-    if (normal_pos(P)) {
-      const double L = pwk::log_pos(P);
+    int bad = 0;
+    const double L = pwk::log_pos_k<LOWP>(P, C, bad);
+    if (!bad) {
       acc[0] = fma(L, w[0], acc[0]);
       acc[1] = fma(L, w[1], acc[1]);
       acc[2] += ax;
@@ -360,6 +369,20 @@ struct Multipole {
 };
 
 // ---------------------------------------------------------------- the tile kernel
+// Functors with per-thread constants (KER::Consts, e.g. the log coefficients) get them
+// built once per thread and passed to every pair.
+struct NoConsts {};
+template <class K, class = void>
+struct HasConsts : std::false_type {
+  using type = NoConsts;
+  __device__ __forceinline__ static type make() { return {}; }
+};
+template <class K>
+struct HasConsts<K, std::void_t<typename K::Consts>> : std::true_type {
+  using type = typename K::Consts;
+  __device__ __forceinline__ static type make() { return K::consts(); }
+};
+
 template <class KER, int NXI, int NROW, int TPT>
 __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_constant__ NearArgs a) {
   __shared__ double s_x[kTile];
@@ -380,6 +403,7 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
     for (int c = 0; c < KER::NACC; ++c) acc[k][c] = 0.0;
   }
   int flag = 0;
+  const typename HasConsts<KER>::type C = HasConsts<KER>::make();
 
   const size_t j_begin = static_cast<size_t>(blockIdx.y) * a.src_per_split;
   size_t j_end = j_begin + a.src_per_split;
@@ -415,7 +439,10 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
 #pragma unroll
       for (int k = 0; k < TPT; ++k) {
         // (t - s) - shift, the reference's association (apply.cpp:534)
-        KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag);
+        if constexpr (HasConsts<KER>::value)
+          KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag, C);
+        else
+          KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag);
       }
     }
   }
@@ -535,7 +562,9 @@ size_t near_outputs(NearKind kind) {
 void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count) {
   if (a.nt == 0 || a.ns == 0) return;
   switch (kind) {
-    case NearKind::Laplace: return dispatch_images<Laplace, 2>(a, st, partial_ws, sm_count);
+    case NearKind::Laplace:
+      return a.lowp ? dispatch_images<Laplace<true>, 2>(a, st, partial_ws, sm_count)
+                    : dispatch_images<Laplace<false>, 2>(a, st, partial_ws, sm_count);
     // precision tier (pw_math.cuh k01_tile): reduced when eps allows it
     case NearKind::ModHelm:
       return a.lowp ? dispatch_images<ModHelm<true>, PWB_MH_TPT>(a, st, partial_ws, sm_count)
@@ -543,8 +572,12 @@ void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* part
     case NearKind::ModHelmGrad:
       return a.lowp ? dispatch_images<ModHelmGrad<true>, PWB_MH_TPT>(a, st, partial_ws, sm_count)
                     : dispatch_images<ModHelmGrad<false>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
-    case NearKind::Stokes: return dispatch_images<Stokes<false>, 1>(a, st, partial_ws, sm_count);
-    case NearKind::StokesP: return dispatch_images<Stokes<true>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::Stokes:
+      return a.lowp ? dispatch_images<Stokes<false, true>, 1>(a, st, partial_ws, sm_count)
+                    : dispatch_images<Stokes<false, false>, 1>(a, st, partial_ws, sm_count);
+    case NearKind::StokesP:
+      return a.lowp ? dispatch_images<Stokes<true, true>, 1>(a, st, partial_ws, sm_count)
+                    : dispatch_images<Stokes<true, false>, 1>(a, st, partial_ws, sm_count);
     case NearKind::ModStokes: return dispatch_images<ModStokes<false>, 1>(a, st, partial_ws, sm_count);
     case NearKind::ModStokesP: return dispatch_images<ModStokes<true>, 1>(a, st, partial_ws, sm_count);
     case NearKind::Stresslet: return dispatch_images<Stresslet, 1>(a, st, partial_ws, sm_count);

@@ -158,11 +158,13 @@ def test_near_and_far_vs_reference(pw, gpu, ref, case, pressure):
             err = rel_l2(got.scalar, want["scalar"], gauge and mode == 1)
         else:
             err = rel_l2(got.velocity, want["velocity"], gauge and mode == 1)
-        tol = 10 * eps if mode == 1 else 1e-13
+        # near images: ~1 ulp kernels, or the reduced tier when eps >= 1e-11 (pw_math.cuh)
+        near_tol = max(1e-13, 1e-4 * eps)
+        tol = 10 * eps if mode == 1 else near_tol
         assert err <= tol, (name, mode, err)
         if pressure:
             perr = rel_l2(got.pressure, want["pressure"], mode == 1)
-            assert perr <= (10 * eps if mode == 1 else 1e-13), (name, mode, "pressure", perr)
+            assert perr <= (10 * eps if mode == 1 else near_tol), (name, mode, "pressure", perr)
 
 
 def test_multipole_and_dlp_vs_reference(pw, gpu, ref):
