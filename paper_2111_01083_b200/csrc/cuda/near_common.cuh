@@ -1,15 +1,10 @@
-// Shared helpers of the near-image tile kernels (near.cu, near_sym.cu).
+// Shared helpers of the near-image tile kernels (near.cu, near_sym_impl.cuh).
 #pragma once
 
 #include "pw_engine.cuh"
 #include "pw_math.cuh"
 
 namespace pwb {
-
-__device__ __forceinline__ bool normal_pos(double p) {
-  const int ex = (pwk::hi_of(p) >> 20) & 0x7ff;
-  return ex != 0 && ex != 0x7ff;
-}
 
 // Fused layouts (every near image, cell.cpp:47-58) have shift.y = n*eta = 0 on the
 // middle row and shift = (0, 0) at its centre; (dy) - 0.0 == dy exactly, so those
