@@ -6,9 +6,7 @@ run() {  # $1 label, $2 flags
   echo "$1 $(grep -o '"near_ms_per_launch": [0-9.]*' gpurun_out/ab_$1.log)"
 }
 run base ""
-run tpt2_m6 "-DPWB_SYM_LAPLACE_TPT=2"
-run tpt8_m3 "-DPWB_SYM_LAPLACE_TPT=8 -DPWB_SYM_LAPLACE_MINB=3"
-run tpt8_m4 "-DPWB_SYM_LAPLACE_TPT=8 -DPWB_SYM_LAPLACE_MINB=4"
-run u1 "-DPWB_SYM_FAST_UNROLL=1"
-run u4 "-DPWB_SYM_FAST_UNROLL=4"
-run tpt4_m5 "-DPWB_SYM_LAPLACE_MINB=5"
+run t2m8 "-DPWB_SYM_LAPLACE_TPT=2 -DPWB_SYM_LAPLACE_MINB=8"
+run t4m7 "-DPWB_SYM_LAPLACE_MINB=7"
+run t2m7 "-DPWB_SYM_LAPLACE_TPT=2 -DPWB_SYM_LAPLACE_MINB=7"
+run t2m8u8 "-DPWB_SYM_LAPLACE_TPT=2 -DPWB_SYM_LAPLACE_MINB=8 -DPWB_SYM_LAPLACE_UNROLL=8"
