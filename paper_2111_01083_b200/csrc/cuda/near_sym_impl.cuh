@@ -142,8 +142,9 @@ struct SymModHelm {
   __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) V[v] = 0.0;
-    // images stay rolled: the Bessel body is long (one copy per image bloated the
-    // instantiations ~10x in code size and compile time for no measurable gain)
+    // rows rolled, image columns unrolled by kSymMhUnrollM: the Bessel body is long (one
+    // copy per image bloated the instantiations ~10x in code size and compile time), but
+    // a few independent chains per thread are needed to hide its latency
 #pragma unroll 1
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);

@@ -116,6 +116,10 @@ KERNEL_CASES = [
     ("stokes-skew", 2, 0.0, (1.0, 0.3, 0.8, 2), 1e-8, "force", True),
     ("stokes-strip", 2, 0.0, (1.0, 0.0, 2.0, 1), 1e-8, "force", True),
     ("mstokes", 3, 1.5, (1.0, 0.2, 0.9, 2), 1e-10, "force", False),
+    # eps < 1e-11: the near tiles run the full precision tier (pw_math.cuh)
+    ("poisson-tight", 0, 0.0, (1.0, 0.1, 1.0, 2), 1e-12, "charge", True),
+    ("stokes-tight", 2, 0.0, (1.0, 0.0, 1.0, 2), 1e-12, "force", True),
+    ("mhelm-tight-strip", 1, 3.0, (1.0, 0.0, 1.2, 1), 1e-12, "charge", False),
 ]
 
 
@@ -478,3 +482,26 @@ def test_symmetric_tile_duplicates_and_image_coincidence(pw, gpu, pde, beta, str
     with pytest.raises(pw.PeriwaveError) as e:
         pw.near_field(pz, pw.ParticleSystem(sources=bad, targets=bad.copy(), **kw))
     assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
+
+
+@pytest.mark.parametrize("pde,strength", [("Poisson", "charge"), ("Stokes", "force"), ("ModHelmholtz", "charge")])
+def test_symmetric_tile_tiers(pw, gpu, pde, strength):
+    """Symmetric tile in both precision tiers (eps = 1e-10 selects the reduced one;
+    PWB_FULL_PRECISION=1 forces the full one) against the one-sided full-tier result."""
+    import os
+
+    rng = np.random.default_rng(7)
+    n = 34000
+    cellt = (1.0, 0.0, 1.0, 2)
+    src, _, kw = _system(rng, cellt, n, 1, strength, pde != "ModHelmholtz")
+    pz = pw.make_periodizer(pw.Pde[pde], 1.5 if pde == "ModHelmholtz" else 0.0, _cell(pw, cellt), 1e-10)
+    key = "scalar" if strength == "charge" else "velocity"
+    os.environ["PWB_FULL_PRECISION"] = "1"
+    try:
+        full_sym = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw)), key)
+        full_one = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), **kw)), key)
+    finally:
+        del os.environ["PWB_FULL_PRECISION"]
+    low_sym = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw)), key)
+    assert rel_l2(full_sym, full_one) <= 1e-13
+    assert rel_l2(low_sym, full_one) <= 1e-12
