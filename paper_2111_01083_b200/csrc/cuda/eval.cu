@@ -136,6 +136,11 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       out[4 * i + 3] = r.k1_over_x * x;
       break;
     }
+    case 8: {  // the reduced tier's table-driven log (pw_math.cuh log_tab), table read unreplicated
+      int bad = 0;
+      out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts(pwk::pw_log_tab64_dev_ptr(), 0, 1), bad);
+      break;
+    }
     default:
       out[i] = nan("");
   }
@@ -192,7 +197,9 @@ double fp64_peak_probe() {
 }
 
 int eval_in_width(int which) { return (which == 0 || which >= 6) ? 1 : which == 5 ? 4 : 2; }
-int eval_out_width(int which) { return which <= 1 ? 1 : (which == 3 || which == 4) ? 2 : which == 6 ? 6 : 4; }
+int eval_out_width(int which) {
+  return (which <= 1 || which == 8) ? 1 : (which == 3 || which == 4) ? 2 : which == 6 ? 6 : 4;
+}
 
 void run_eval(int which, int pde, double beta, int l, size_t n, const double* in_host, double* out_host) {
   const size_t nin = n * eval_in_width(which), nout = n * eval_out_width(which);

@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "near_common.cuh"
 #include "pw_engine.cuh"
@@ -51,6 +52,9 @@ namespace sym {
 #endif
 #ifndef PWB_SYM_LAPLACE_UNROLL
 #define PWB_SYM_LAPLACE_UNROLL 4  // sources per unrolled step of the fast loop (c4: 904 -> 895 ms vs 2)
+#endif
+#ifndef PWB_SYM_LOG_TABLE
+#define PWB_SYM_LOG_TABLE 1  // reduced tier: table-driven ln (pw_math.cuh log_tab) instead of log_pos_k<true>
 #endif
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
@@ -86,9 +90,9 @@ struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT, CHUNK = 8,
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_;
-  template <int NXI, int NROW>
+  template <int NXI, int NROW, class LK>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const pwk::LogK<LOWP>& K, int& bad) {
+                                                     const LK& K, int& bad) {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -103,7 +107,7 @@ struct SymLaplace {
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         P *= fma(rx, rx, ry2[n]);
       }
-    V[0] = pwk::log_pos_k(P, K, bad);
+    V[0] = pwk::log_fast(P, K, bad);
   }
   template <int NXI, int NROW>
   __device__ __noinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
@@ -135,9 +139,8 @@ template <bool GRAD, bool LOWP_>
 struct SymModHelm {
   static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0, UNROLL = 1;
   static constexpr bool FAST = false, LOWP = LOWP_;
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&,
-                                                     const pwk::LogK<LOWP>&, int&) {}
+  template <int NXI, int NROW, class LK>
+  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, int&) {}
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
 #pragma unroll
@@ -199,9 +202,9 @@ struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
                        CHUNK = 16, MINB = 0, UNROLL = 2;
   static constexpr bool FAST = true, LOWP = LOWP_;
-  template <int NXI, int NROW>
+  template <int NXI, int NROW, class LK>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const pwk::LogK<LOWP>& K, int& bad) {
+                                                     const LK& K, int& bad) {
     double P = 1.0, txx = 0.0, txy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -222,7 +225,7 @@ struct SymStokes {
         }
       }
     }
-    V[0] = pwk::log_pos_k(P, K, bad);
+    V[0] = pwk::log_fast(P, K, bad);
     V[1] = txx;
     V[2] = txy;
     // rx^2/r^2 + ry^2/r^2 = 1 per image (no exact zero on this path): trace = image count,
@@ -342,8 +345,19 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     for (int c = 0; c < K::NACC; ++c) racc[k][c] = 0.0;
   }
   int flag = 0;
-  pwk::LogK<K::LOWP> LK;
-  if (K::FAST) LK = pwk::log_consts<K::LOWP>();
+  // log constants in registers; the reduced tier's log table in shared memory
+  constexpr size_t kTileSmem = sizeof(double) * (static_cast<size_t>(TILE) * (2 + K::NW) + kWarps * K::NACC * TILE);
+  constexpr size_t kTabSmem = sizeof(double2) * pwk::kLogTabEntries * pwk::kLogTabReplicas;
+  constexpr bool kTab = K::FAST && K::LOWP && PWB_SYM_LOG_TABLE && kTileSmem + kTabSmem <= 48 * 1024;
+  __shared__ double2 s_lt[kTab ? pwk::kLogTabEntries * pwk::kLogTabReplicas : 1];
+  using LKT = std::conditional_t<kTab, pwk::LogT, pwk::LogK<K::LOWP>>;
+  LKT LK;
+  if constexpr (kTab) {
+    pwk::log_tab_fill(s_lt, tid, kT);  // visible after the first __syncthreads of the tile loop
+    LK = pwk::log_tab_consts(s_lt, lane);
+  } else if constexpr (K::FAST) {
+    LK = pwk::log_consts<K::LOWP>();
+  }
 
   for (int J = J0; J < J1; ++J) {
     const size_t jbase = static_cast<size_t>(J) * TILE;
