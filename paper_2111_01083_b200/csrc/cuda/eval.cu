@@ -137,8 +137,8 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       break;
     }
     case 8: {  // the reduced tier's table-driven log (pw_math.cuh log_tab), table read unreplicated
-      int bad = 0;
-      out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts(pwk::pw_log_tab64_dev_ptr(), 0, 1), bad);
+      unsigned bad = 0;
+      out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts(pwk::pw_log_tab64_dev_ptr(), 0), bad);
       break;
     }
     default:

@@ -90,9 +90,9 @@ struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT, CHUNK = 8,
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_;
-  template <int NXI, int NROW, class LK>
+  template <int NXI, int NROW, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const LK& K, int& bad) {
+                                                     const LK& K, B& bad) {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -139,8 +139,8 @@ template <bool GRAD, bool LOWP_>
 struct SymModHelm {
   static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0, UNROLL = 1;
   static constexpr bool FAST = false, LOWP = LOWP_;
-  template <int NXI, int NROW, class LK>
-  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, int&) {}
+  template <int NXI, int NROW, class LK, class B>
+  __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
   template <int NXI, int NROW>
   __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
 #pragma unroll
@@ -202,9 +202,9 @@ struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
                        CHUNK = 16, MINB = 0, UNROLL = 2;
   static constexpr bool FAST = true, LOWP = LOWP_;
-  template <int NXI, int NROW, class LK>
+  template <int NXI, int NROW, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
-                                                     const LK& K, int& bad) {
+                                                     const LK& K, B& bad) {
     double P = 1.0, txx = 0.0, txy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
@@ -400,7 +400,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       for (int k = 0; k < TPT; ++k)
 #pragma unroll
         for (int c = 0; c < K::NACC; ++c) keep[k][c] = racc[k][c];
-      int bad = 0;
+      std::conditional_t<kTab, unsigned, int> bad = 0;  // see pwk::log_bad
 #pragma unroll K::UNROLL
       for (int i = 0; i < TILE; ++i) {
         const int jj = (lane + i) & (TILE - 1);
@@ -422,7 +422,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
       }
-      if (__syncthreads_or(bad)) {  // rare: redo this tile on the careful path
+      if (__syncthreads_or(pwk::log_bad(LK, bad))) {  // rare: redo this tile on the careful path
 #pragma unroll
         for (int k = 0; k < TPT; ++k)
 #pragma unroll
