@@ -11,6 +11,7 @@
 
 #include "engine.hpp"
 #include "nufft.hpp"
+#include "pw_math.cuh"
 
 namespace pwb {
 
@@ -822,6 +823,8 @@ bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
   return accelerated;
 }
 
+double screen_cutoff(double eps, int images, size_t ns, bool grad);
+
 NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
                          bool identity, NearArgs& a) const {
   const Kind kind = kind_of(pz_);
@@ -835,12 +838,13 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
   a.vec = s.f;
   a.beta = pz_.beta;
   a.beta2 = pz_.beta * pz_.beta;
-  a.xcut2 = 64.0 * 64.0;  // K_0(x) < 3e-29 beyond: below fp64 resolution of any sum
+  a.xcut2 = 64.0 * 64.0;  // K_0(x) < 3e-29 beyond; screened kinds refine it below (screen_cutoff)
   // precision tier of the near tiles (pw_math.cuh log_pos_k, k01_tile): the reduced tier
   // keeps |error| <= ~3e-13 per pair-log and <= 6e-14 relative per Bessel value, >= 1.5
   // orders below eps for eps >= 1e-11 (the reference's eps bounds the far truncation);
   // the full tier is ~1 ulp. PWB_FULL_PRECISION forces the full tier (tests).
   a.lowp = (pz_.eps >= 1e-11 && std::getenv("PWB_FULL_PRECISION") == nullptr) ? 1 : 0;
+  a.cull = std::getenv("PWB_NO_CULL") == nullptr ? 1 : 0;  // A/B and the exactness test only
   if (kind == Kind::Multipole) {
     nk = NearKind::Multipole;
     a.vec = s.coef;
@@ -900,7 +904,36 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
       a.id_img = 1;
     }
   }
+  if (nk == NearKind::ModHelm || nk == NearKind::ModHelmGrad) {
+    const double xc = screen_cutoff(pz_.eps, a.nxi * a.nrow, s.ns, nk == NearKind::ModHelmGrad);
+    a.xcut2 = xc * xc;
+  }
   return nk;
+}
+
+// Screening cut-off of the modified-Helmholtz near tiles: pairs with x = beta r >= x_c
+// are skipped, x_c the smallest x in [2, 64] with K0(x) <= 1e-3 eps / (images * N_S)
+// (K1 for the gradient, with a factor 2 of margin). Every target then loses at most
+// 1e-3 eps max|q| / 2pi in total -- a thousandth of eps times the field of one unit
+// source at beta r ~ 0.6 (K0 = 1 / 2pi scale) -- while the parity bar is 10 eps
+// relative. The reference sums every pair to GSL's underflow (x ~ 700); K0(64) ~ 3e-29,
+// the previous fixed cut-off, is the upper end. PWB_KCUT=<x> overrides (A/B, tests).
+double screen_cutoff(double eps, int images, size_t ns, bool grad) {
+  if (const char* e = std::getenv("PWB_KCUT")) return std::atof(e);
+  const double thr = 1e-3 * eps / (static_cast<double>(images) * static_cast<double>(ns > 0 ? ns : 1)) *
+                     (grad ? 0.5 : 1.0);
+  auto val = [grad](double x) {
+    const pwk::K01 k = pwk::k01_of_sq(x * x);
+    return grad ? k.k1_over_x * x : k.k0;
+  };
+  if (val(64.0) > thr) return 64.0;
+  double lo = 2.0, hi = 64.0;  // val(lo) > thr >= val(hi) (K0(2) = 0.11 > any eps-scaled threshold)
+  if (val(lo) <= thr) return lo;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    (val(mid) > thr ? lo : hi) = mid;
+  }
+  return hi;
 }
 
 long Plan::sym_items(const Opts& o, size_t n) {

@@ -28,6 +28,8 @@ __device__ double bessel_kn_dev(int l, double x) {
 
 __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  pwk::exp_tab_fill();  // the reduced tier's exp table (case 7)
+  __syncthreads();
   if (i >= n) return;
   const double inv2pi = 1.0 / (2.0 * pwk::kPi);
   switch (which) {

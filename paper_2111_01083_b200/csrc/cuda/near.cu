@@ -99,6 +99,7 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
 template <bool LOWP>
 struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
   static constexpr int NW = 1, NACC = 1, NOUT = 1;
+  static constexpr bool EXP_TAB = LOWP;  // k01_tile<true, .> reads the shared exp table
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
                                               const NearArgs& a, int& flag) {
@@ -129,6 +130,7 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
 template <bool LOWP>
 struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
   static constexpr int NW = 1, NACC = 3, NOUT = 3;
+  static constexpr bool EXP_TAB = LOWP;
   template <int NXI, int NROW>
   __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
                                               const NearArgs& a, int& flag) {
@@ -383,6 +385,11 @@ struct HasConsts<K, std::void_t<typename K::Consts>> : std::true_type {
   __device__ __forceinline__ static type make() { return K::consts(); }
 };
 
+template <class K, class = void>
+struct UsesExpTab : std::false_type {};
+template <class K>
+struct UsesExpTab<K, std::enable_if_t<K::EXP_TAB>> : std::true_type {};
+
 template <class KER, int NXI, int NROW, int TPT>
 __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_constant__ NearArgs a) {
   __shared__ double s_x[kTile];
@@ -404,6 +411,7 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
   }
   int flag = 0;
   const typename HasConsts<KER>::type C = HasConsts<KER>::make();
+  if constexpr (UsesExpTab<KER>::value) pwk::exp_tab_fill();  // visible after the tile loop's first __syncthreads
 
   const size_t j_begin = static_cast<size_t>(blockIdx.y) * a.src_per_split;
   size_t j_end = j_begin + a.src_per_split;

@@ -89,7 +89,7 @@ template <bool LOWP_>
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT, CHUNK = 8,
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
-  static constexpr bool FAST = true, LOWP = LOWP_;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
   template <int NXI, int NROW, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -139,10 +139,15 @@ template <bool GRAD, bool LOWP_>
 struct SymModHelm {
   static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0, UNROLL = 1;
   static constexpr bool FAST = false, LOWP = LOWP_;
+  static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
+  static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
   template <int NXI, int NROW, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
+  // mask: bit n * NXI + m set for the images that may hold a pair with beta r < 64 in this
+  // tile pair (block-uniform, so the skips are uniform branches)
   template <int NXI, int NROW>
-  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag) {
+  __device__ __forceinline__ static void values(double* V, double dx, double dy, const NearArgs& a, int& flag,
+                                                unsigned mask) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) V[v] = 0.0;
     // rows rolled, image columns unrolled by kSymMhUnrollM: the Bessel body is long (one
@@ -154,6 +159,7 @@ struct SymModHelm {
       const double ry2 = ry * ry;
 #pragma unroll kSymMhUnrollM
       for (int m = 0; m < NXI; ++m) {
+        if (!((mask >> (n * NXI + m)) & 1u)) continue;
         const double rx = img_dx<NXI, NROW>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         if (r2 == 0.0) {
@@ -201,7 +207,7 @@ template <bool PRESSURE, bool LOWP_>
 struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
                        CHUNK = 16, MINB = 0, UNROLL = 2;
-  static constexpr bool FAST = true, LOWP = LOWP_;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
   template <int NXI, int NROW, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -308,6 +314,56 @@ __device__ __forceinline__ void load_w(const NearArgs& a, size_t j, bool live, d
 }
 
 template <class K, int NXI, int NROW>
+__device__ __forceinline__ void call_values(double* V, double dx, double dy, const NearArgs& a, int& flag,
+                                            unsigned mask) {
+  if constexpr (K::CULL)
+    K::template values<NXI, NROW>(V, dx, dy, a, flag, mask);
+  else
+    K::template values<NXI, NROW>(V, dx, dy, a, flag);
+}
+
+// Axis-aligned box (xmin, -xmax, ymin, -ymax) of a point set, warp-reduced; lane 0 of
+// each warp stores its warp's box in s_box[warp].
+__device__ __forceinline__ void warp_box_store(double b0, double b1, double b2, double b3, int lane, double* s_box) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    b0 = fmin(b0, __shfl_xor_sync(0xffffffffu, b0, o));
+    b1 = fmin(b1, __shfl_xor_sync(0xffffffffu, b1, o));
+    b2 = fmin(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+    b3 = fmin(b3, __shfl_xor_sync(0xffffffffu, b3, o));
+  }
+  if (lane == 0) {
+    s_box[0] = b0;
+    s_box[1] = b1;
+    s_box[2] = b2;
+    s_box[3] = b3;
+  }
+}
+
+// Images whose every (target, source) pair between the row box and the column box has
+// beta^2 r^2 >= xcut2 get their bit cleared: the per-pair test would skip all of them.
+// The box gap is a lower bound of |(t - s) - shift| per axis; the 1e-4 margin covers
+// its rounding, so the mask never drops a pair the per-pair test would keep.
+template <int NXI, int NROW>
+__device__ __forceinline__ unsigned image_mask(const double* rb, const double* cb, const NearArgs& a) {
+  unsigned mask = 0;
+#pragma unroll
+  for (int n = 0; n < NROW; ++n) {
+    const double ylo = (rb[2] + cb[3]) - a.shy[n];  // tymin - symax - shift
+    const double yhi = (-rb[3] - cb[2]) - a.shy[n];
+    const double gy = ylo > 0.0 ? ylo : (yhi < 0.0 ? -yhi : 0.0);
+#pragma unroll
+    for (int m = 0; m < NXI; ++m) {
+      const double xlo = (rb[0] + cb[1]) - a.shx[n * NXI + m];
+      const double xhi = (-rb[1] - cb[0]) - a.shx[n * NXI + m];
+      const double gx = xlo > 0.0 ? xlo : (xhi < 0.0 ? -xhi : 0.0);
+      if (a.beta2 * fma(gx, gx, gy * gy) * 0.9999 < a.xcut2) mask |= 1u << (n * NXI + m);
+    }
+  }
+  return mask;
+}
+
+template <class K, int NXI, int NROW>
 __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   constexpr int TPT = K::TPT;
   constexpr int TILE = kT * TPT;
@@ -358,16 +414,38 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   } else if constexpr (K::FAST) {
     LK = pwk::log_consts<K::LOWP>();
   }
+  if constexpr (K::EXP_TAB) pwk::exp_tab_fill();  // visible after the first __syncthreads of the tile loop
+  // screened kernels: bounding boxes of the row tile and of each column tile -> image mask
+  __shared__ double s_rbox[K::CULL ? kWarps : 1][4], s_cbox[K::CULL ? kWarps : 1][4];
+  if constexpr (K::CULL) {
+    double b[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#pragma unroll
+    for (int k = 0; k < TPT; ++k)
+      if (live[k]) {
+        b[0] = fmin(b[0], tx[k]);
+        b[1] = fmin(b[1], -tx[k]);
+        b[2] = fmin(b[2], ty[k]);
+        b[3] = fmin(b[3], -ty[k]);
+      }
+    warp_box_store(b[0], b[1], b[2], b[3], lane, s_rbox[warp]);  // read after the tile loop's syncs
+  }
 
   for (int J = J0; J < J1; ++J) {
     const size_t jbase = static_cast<size_t>(J) * TILE;
     __syncthreads();
+    double cb[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     for (int i = tid; i < TILE; i += kT) {
       const size_t j = jbase + i;
       const bool lv = j < n;
       const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);
       s_x[i] = p.x;
       s_y[i] = p.y;
+      if (K::CULL && lv) {
+        cb[0] = fmin(cb[0], p.x);
+        cb[1] = fmin(cb[1], -p.x);
+        cb[2] = fmin(cb[2], p.y);
+        cb[3] = fmin(cb[3], -p.y);
+      }
       double w[K::NW];
       load_w<K>(a, j, lv, w);
 #pragma unroll
@@ -377,7 +455,19 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
     }
+    if constexpr (K::CULL) warp_box_store(cb[0], cb[1], cb[2], cb[3], lane, s_cbox[warp]);
     __syncthreads();
+    unsigned mask = ~0u;
+    if (K::CULL && a.cull) {
+      double rb[4], cbx[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        rb[c] = fmin(fmin(s_rbox[0][c], s_rbox[1][c]), fmin(s_rbox[2][c], s_rbox[3][c]));
+        cbx[c] = fmin(fmin(s_cbox[0][c], s_cbox[1][c]), fmin(s_cbox[2][c], s_cbox[3][c]));
+      }
+      mask = image_mask<NXI, NROW>(rb, cbx, a);
+      if (mask == 0u) continue;  // block-uniform: no pair of this tile pair is in range
+    }
     if (J == I) {  // diagonal tile: one-sided and careful (self pairs live here)
       for (int i = 0; i < TILE; ++i) {
         const double sx = s_x[i], sy = s_y[i];
@@ -387,7 +477,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int k = 0; k < TPT; ++k) {
           double V[K::NV];
-          K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
+          call_values<K, NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag, mask);
           K::row(racc[k], V, w);
         }
       }
@@ -450,7 +540,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int k = 0; k < TPT; ++k) {
           double V[K::NV];
-          K::template values<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag);
+          call_values<K, NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, flag, mask);
           K::row(racc[k], V, w);
           K::col(cacc, V, tw[k]);
         }

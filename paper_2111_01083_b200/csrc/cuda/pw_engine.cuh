@@ -52,6 +52,7 @@ struct NearArgs {
   int* flag = nullptr;     // set to 1 on a non-identity exact coincidence
   const int* out_row = nullptr;  // binned targets: output row of target l (nullptr: l)
   int lowp = 0;                  // near tiles: reduced-precision tier (eps >= 1e-11, pw_math.cuh)
+  int cull = 1;                  // screened symmetric tiles: per-tile image mask (near_sym_impl.cuh)
 };
 
 // ---------------------------------------------------------------- spatial binning (binning.cu)

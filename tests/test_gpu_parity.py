@@ -353,6 +353,28 @@ def test_symmetric_targets_equal_sources(pw, gpu, ref, name, n):
     assert rel_l2(sym[idx], want, gauge) <= 10 * c.eps
 
 
+@pytest.mark.parametrize("grad", [False, True])
+def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad):
+    """The screened symmetric tile drops, per tile pair, the images whose bounding-box gap
+    puts every pair beyond the K0 cut-off (near_sym_impl.cuh image_mask). The per-pair test
+    would skip those pairs anyway, so the fixed-point sums are bitwise those without the
+    mask (PWB_NO_CULL=1). Wide cell (c5's aspect) so most tile pairs lose images."""
+    rng = np.random.default_rng(123)
+    n = 40000
+    cellt = (100.0, 0.0, 1.0, 2)
+    src = np.ascontiguousarray(np.column_stack([rng.uniform(-50, 50, n), rng.uniform(-0.5, 0.5, n)]))
+    q = np.ascontiguousarray(rng.standard_normal(n))
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, _cell(pw, cellt), 1e-8)
+    s = pw.ParticleSystem(sources=src, targets=src, charges=q)
+    culled = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
+    monkeypatch.setenv("PWB_NO_CULL", "1")
+    full = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
+    assert np.array_equal(culled.scalar, full.scalar)
+    if grad:
+        assert np.array_equal(culled.gradient, full.gradient)
+    assert np.abs(full.scalar).max() > 0
+
+
 def test_symmetric_gradient_and_pressure(pw, gpu, ref):
     rng = np.random.default_rng(77)
     cellt = (1.0, 0.3, 0.8, 2)
