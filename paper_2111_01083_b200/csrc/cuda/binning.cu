@@ -45,6 +45,16 @@ __global__ void gather_kernel(const T* __restrict__ in, const int* __restrict__ 
 
 unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
+// out[perm[i] * w + k] += in[i * w + k]: sorted-order fixed-point rows back to input order
+// (integer adds: exact; perm is a permutation, so no two threads touch the same row)
+__global__ void scatter_add_rows_kernel(const unsigned long long* __restrict__ in, const int* __restrict__ perm,
+                                        size_t n, int w, unsigned long long* __restrict__ out) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * static_cast<size_t>(w)) return;
+  const size_t row = i / w;
+  out[static_cast<size_t>(perm[row]) * w + (i - row * w)] += in[i];
+}
+
 }  // namespace
 
 size_t morton_order_bytes(size_t n) {
@@ -80,6 +90,13 @@ void morton_order(const double2* pts, size_t n, const BinBox& box, int* perm, vo
 void gather_double(const double* in, const int* perm, size_t n, double* out, cudaStream_t st) {
   if (n == 0 || in == nullptr) return;
   gather_kernel<double><<<blocks_for(n), 256, 0, st>>>(in, perm, n, out);
+  count_launches(1);
+}
+
+void scatter_add_rows(const unsigned long long* in, const int* perm, size_t n, int width, unsigned long long* out,
+                      cudaStream_t st) {
+  if (n == 0) return;
+  scatter_add_rows_kernel<<<blocks_for(n * width), 256, 0, st>>>(in, perm, n, width, out);
   count_launches(1);
 }
 

@@ -824,6 +824,7 @@ bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
 }
 
 double screen_cutoff(double eps, int images, size_t ns, bool grad);
+bool near_screened(NearKind nk, const NearArgs& a);
 
 NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
                          bool identity, NearArgs& a) const {
@@ -968,7 +969,23 @@ void Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, uns
   r.end = end;
   r.finish = false;
   cuda_check(cudaEventRecord(ev_[2], st), "event");
-  launch_near_sym(nk, a, st, acc, rs_dev, rs_host, r);
+  // screened kernels: the same Morton binning as the single-GPU path (every rank sorts the
+  // same points identically, so the work items cover the same pairs); the tile runs into a
+  // sorted-order scratch accumulator that is added back in input order, keeping the
+  // accumulator layout (and the reduce-scatter slices) of the caller
+  if (near_screened(nk, a) && s.nt >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr) {
+    bin_inputs(s, a, st);
+    const int* perm = a.out_row;
+    a.out_row = nullptr;
+    const int w = 3 * static_cast<int>(near_outputs(nk));
+    auto* sorted = sym_fx_.as<unsigned long long>(static_cast<size_t>(w) * s.nt);
+    cuda_check(cudaMemsetAsync(sorted, 0, static_cast<size_t>(w) * s.nt * sizeof(unsigned long long), st),
+               "memset sorted acc");
+    launch_near_sym(nk, a, st, sorted, rs_dev, rs_host, r);
+    scatter_add_rows(sorted, perm, s.nt, w, acc, st);
+  } else {
+    launch_near_sym(nk, a, st, acc, rs_dev, rs_host, r);
+  }
   cuda_check(cudaEventRecord(ev_[3], st), "event");
   near_timed_ = true;
   cuda_check(cudaGetLastError(), "near launch");
@@ -984,6 +1001,11 @@ void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, 
   launch_fx_finish(acc, n, a.out0, a.nout0, a.out1, a.nout1, nullptr, stream_for(o));
   cuda_check(cudaGetLastError(), "fixed-point finish");
   cuda_check(cudaStreamSynchronize(stream_for(o)), "sync");
+}
+
+bool near_screened(NearKind nk, const NearArgs& a) {
+  return nk == NearKind::ModHelm || nk == NearKind::ModHelmGrad || nk == NearKind::ModStokes ||
+         nk == NearKind::ModStokesP || (nk == NearKind::Multipole && a.screened);
 }
 
 // Morton-ordered copies of the points and strengths; outputs keep their original
@@ -1048,8 +1070,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
                          std::getenv("PWB_NO_SYMMETRIC") == nullptr;
   cuda_check(cudaEventRecord(ev_[2], st), "event");
   // screened kernels branch on beta*r per pair: bin so the branch is warp-uniform
-  const bool screened = nk == NearKind::ModHelm || nk == NearKind::ModHelmGrad || nk == NearKind::ModStokes ||
-                        nk == NearKind::ModStokesP || (nk == NearKind::Multipole && a.screened);
+  const bool screened = near_screened(nk, a);
   if (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)
     bin_inputs(s, a, st);
   bool done = false;

@@ -65,6 +65,9 @@ void morton_order(const double2* pts, size_t n, const BinBox& box, int* perm, vo
                   cudaStream_t st);
 void gather_double(const double* in, const int* perm, size_t n, double* out, cudaStream_t st);
 void gather_double2(const double2* in, const int* perm, size_t n, double2* out, cudaStream_t st);
+// out[perm[i]] += in[i] row-wise (width uint64 per row): sorted fixed-point rows -> input order
+void scatter_add_rows(const unsigned long long* in, const int* perm, size_t n, int width, unsigned long long* out,
+                      cudaStream_t st);
 
 size_t near_outputs(NearKind kind);
 void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count);

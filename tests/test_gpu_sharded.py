@@ -8,12 +8,19 @@ from conftest import rel_l2
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("binning", [True, False])
 @pytest.mark.parametrize("name,n,pressure", [("c4", 40000, False), ("c3", 33000, True), ("c5", 34000, False)])
-def test_symmetric_items_compose_bitwise(pw, gpu, name, n, pressure):
+def test_symmetric_items_compose_bitwise(pw, gpu, monkeypatch, name, n, pressure, binning):
+    """Work items split across 2 or 3 simulated ranks add up (int64) to the single call,
+    bitwise. Screened kernels (c5) bin on both paths: every rank sorts the same points the
+    same way and adds its sorted-order accumulator back in input order (engine.cu
+    sym_partial); PWB_NO_BINNING=1 runs both in input order."""
     import torch
 
     from paper_2111_01083_b200 import configs, dist as pdist
 
+    if not binning:
+        monkeypatch.setenv("PWB_NO_BINNING", "1")
     inp = configs.generate(name, n_src=n)
     c = inp.config
     pz = pw.make_periodizer(c.pde, c.beta, pw.make_unit_cell(*c.cell[:3], c.cell[3]), c.eps)
@@ -21,15 +28,8 @@ def test_symmetric_items_compose_bitwise(pw, gpu, name, n, pressure):
     src = torch.from_numpy(inp.sources).cuda()
     q = torch.from_numpy(inp.charges if kw == "charges" else inp.forces).cuda()
     opt = pw.ApplyOptions(with_pressure=pressure)
-    # n above the symmetric-tile threshold (32768), so the single call takes the same tile;
-    # the sharded items run in input order, so the single call must not bin (binning.cu)
-    import os
-
-    os.environ["PWB_NO_BINNING"] = "1"
-    try:
-        whole = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **{kw: q}), opt)
-    finally:
-        del os.environ["PWB_NO_BINNING"]
+    # n above the symmetric-tile threshold (32768), so the single call takes the same tile
+    whole = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **{kw: q}), opt)
     items, nout = pw.near_sym_items(pz, n, opt)
     for world in (2, 3):
         acc = torch.zeros(n * nout * 3, dtype=torch.int64, device="cuda")
