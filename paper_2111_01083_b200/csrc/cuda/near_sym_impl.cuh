@@ -180,6 +180,26 @@ struct SymModHelm {
       }
     }
   }
+  // One image of one pair for the image-outer loop of the off-diagonal tiles: false when
+  // the pair contributes nothing (beyond the cut-off, or an exact zero -- skipped in the
+  // identity image, flagged in any other, apply.cpp:538-545).
+  __device__ __forceinline__ static bool image_value(double* V, double rx, double ry, bool ident,
+                                                     const NearArgs& a, int& flag) {
+    const double r2 = fma(rx, rx, ry * ry);
+    if (r2 == 0.0 && rx == 0.0 && ry == 0.0) {
+      if (!ident) flag = 1;
+      return false;
+    }
+    const double X = a.beta2 * r2;
+    if (!(X < a.xcut2)) return false;
+    const pwk::K01 k = pwk::k01_tile<LOWP, GRAD>(X);
+    V[0] = k.k0;
+    if (GRAD) {
+      V[1] = k.k1_over_x * rx;
+      V[2] = k.k1_over_x * ry;
+    }
+    return true;
+  }
   __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v] = fma(w[0], V[v], acc[v]);
@@ -484,6 +504,41 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       continue;
     }
     bool careful = !K::FAST;
+    if constexpr (K::CULL) {
+      // Screened tiles, off-diagonal: image-outer order. The image's shift is loop-invariant
+      // and its mask bit is tested once per tile pair, the inner loop is one K0 (K1) per
+      // (target, source) -- small code, two sources in flight -- and the column partials
+      // take one shared-memory update per (image, source).
+#pragma unroll 1
+      for (int img = 0; img < NXI * NROW; ++img) {
+        if (!((mask >> img) & 1u)) continue;
+        const double shx = a.shx[img], shy = a.shy[img / NXI];
+        const bool ident = img == a.id_img;
+#pragma unroll 2
+        for (int i = 0; i < TILE; ++i) {
+          const int jj = (lane + i) & (TILE - 1);
+          const double sx = s_x[jj], sy = s_y[jj];
+          double w[K::NW];
+#pragma unroll
+          for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+          double cacc[K::NACC];
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+#pragma unroll
+          for (int k = 0; k < TPT; ++k) {
+            double V[K::NV];
+            // (t - s) - shift as upstream (apply.cpp:534)
+            if (K::image_value(V, (tx[k] - sx) - shx, (ty[k] - sy) - shy, ident, a, flag)) {
+              K::row(racc[k], V, w);
+              K::col(cacc, V, tw[k]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+        }
+      }
+      careful = false;
+    }
     if (K::FAST) {
       double keep[TPT][K::NACC];
 #pragma unroll
