@@ -907,7 +907,9 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
   }
   if (nk == NearKind::ModHelm || nk == NearKind::ModHelmGrad) {
     const double xc = screen_cutoff(pz_.eps, a.nxi * a.nrow, s.ns, nk == NearKind::ModHelmGrad);
-    a.xcut2 = xc * xc;
+    // round x_c^2 up to a zero low word: the tiles compare high words on the integer pipe
+    // (pw_math.cuh lt_hi), exact for such a bound
+    a.xcut2 = pwk::hi_lo(pwk::hi_of(xc * xc) + (pwk::lo_of(xc * xc) != 0u ? 1 : 0), 0u);
   }
   return nk;
 }

@@ -122,6 +122,20 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
       }
     }
   }
+  // one image of one pair (image-outer loop of near_tile_kernel): same semantics as pair()
+  static constexpr bool IMAGE_OUTER = true;
+  __device__ __forceinline__ static void image(double* acc, double rx, double ry, const double* w, bool ident,
+                                               const NearArgs& a, int& flag) {
+    const double r2 = fma(rx, rx, ry * ry);
+    // r2 < 2^-1022 (integer test on the high word) is rare; only an exact zero of the
+    // shifted delta is a coincidence
+    if (pwk::hi_of(r2) < 0x00100000 && rx == 0.0 && ry == 0.0) {
+      if (!ident) flag = 1;
+      return;
+    }
+    const double X = a.beta2 * r2;
+    if (pwk::lt_hi(X, a.xcut2)) acc[0] = fma(w[0], pwk::k01_tile<LOWP, false>(X).k0, acc[0]);
+  }
   __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
     out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
   }
@@ -157,6 +171,25 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
           acc[2] = fma(g, ry, acc[2]);
         }
       }
+    }
+  }
+  static constexpr bool IMAGE_OUTER = true;
+  __device__ __forceinline__ static void image(double* acc, double rx, double ry, const double* w, bool ident,
+                                               const NearArgs& a, int& flag) {
+    const double r2 = fma(rx, rx, ry * ry);
+    // r2 < 2^-1022 (integer test on the high word) is rare; only an exact zero of the
+    // shifted delta is a coincidence
+    if (pwk::hi_of(r2) < 0x00100000 && rx == 0.0 && ry == 0.0) {
+      if (!ident) flag = 1;
+      return;
+    }
+    const double X = a.beta2 * r2;
+    if (pwk::lt_hi(X, a.xcut2)) {
+      const pwk::K01 k = pwk::k01_tile<LOWP, true>(X);
+      acc[0] = fma(w[0], k.k0, acc[0]);
+      const double g = w[0] * k.k1_over_x;
+      acc[1] = fma(g, rx, acc[1]);
+      acc[2] = fma(g, ry, acc[2]);
     }
   }
   __device__ __forceinline__ static void finish(const double* acc, const NearArgs& a, double* out) {
@@ -386,6 +419,11 @@ struct HasConsts<K, std::void_t<typename K::Consts>> : std::true_type {
 };
 
 template <class K, class = void>
+struct ImageOuter : std::false_type {};
+template <class K>
+struct ImageOuter<K, std::enable_if_t<K::IMAGE_OUTER>> : std::true_type {};
+
+template <class K, class = void>
 struct UsesExpTab : std::false_type {};
 template <class K>
 struct UsesExpTab<K, std::enable_if_t<K::EXP_TAB>> : std::true_type {};
@@ -438,6 +476,26 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
       }
     }
     __syncthreads();
+    if constexpr (ImageOuter<KER>::value) {
+      // screened kernels: image-outer order (loop-invariant shift, one K0 per inner
+      // iteration, small code; near_sym_impl.cuh does the same on its off-diagonal tiles)
+#pragma unroll 1
+      for (int img = 0; img < NXI * NROW; ++img) {
+        const double shx = a.shx[img], shy = a.shy[img / NXI];
+        const bool ident = img == a.id_img;
+#pragma unroll 2
+        for (int i = 0; i < tn; ++i) {
+          const double sx = s_x[i], sy = s_y[i];
+          double w[KER::NW];
+#pragma unroll
+          for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
+#pragma unroll
+          for (int k = 0; k < TPT; ++k)  // (t - s) - shift, the reference's association (apply.cpp:534)
+            KER::image(acc[k], (tx[k] - sx) - shx, (ty[k] - sy) - shy, w, ident, a, flag);
+        }
+      }
+      continue;
+    }
 #pragma unroll 2
     for (int i = 0; i < tn; ++i) {
       const double sx = s_x[i], sy = s_y[i];

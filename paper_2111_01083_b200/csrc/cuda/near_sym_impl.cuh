@@ -186,12 +186,14 @@ struct SymModHelm {
   __device__ __forceinline__ static bool image_value(double* V, double rx, double ry, bool ident,
                                                      const NearArgs& a, int& flag) {
     const double r2 = fma(rx, rx, ry * ry);
-    if (r2 == 0.0 && rx == 0.0 && ry == 0.0) {
+    // r2 < 2^-1022 (integer test on the high word) is rare; only an exact zero of the
+    // shifted delta is a coincidence
+    if (pwk::hi_of(r2) < 0x00100000 && rx == 0.0 && ry == 0.0) {
       if (!ident) flag = 1;
       return false;
     }
     const double X = a.beta2 * r2;
-    if (!(X < a.xcut2)) return false;
+    if (!pwk::lt_hi(X, a.xcut2)) return false;  // xcut2 has a zero low word (engine.cu)
     const pwk::K01 k = pwk::k01_tile<LOWP, GRAD>(X);
     V[0] = k.k0;
     if (GRAD) {
@@ -199,6 +201,18 @@ struct SymModHelm {
       V[2] = k.k1_over_x * ry;
     }
     return true;
+  }
+  // Same value as image_value for a pair known to be in asymptotic regime FAR (near if
+  // false) and inside the cut-off (pw_math.cuh regime_of): branch-free.
+  template <bool FAR>
+  __device__ __forceinline__ static void image_fast(double* V, double rx, double ry, const NearArgs& a) {
+    const double X = a.beta2 * fma(rx, rx, ry * ry);
+    const pwk::K01 k = pwk::k01_asym<LOWP, GRAD, FAR>(X);
+    V[0] = k.k0;
+    if (GRAD) {
+      V[1] = k.k1_over_x * rx;
+      V[2] = k.k1_over_x * ry;
+    }
   }
   __device__ __forceinline__ static void row(double* acc, const double* V, const double* w) {
 #pragma unroll
@@ -342,24 +356,6 @@ __device__ __forceinline__ void call_values(double* V, double dx, double dy, con
     K::template values<NXI, NROW>(V, dx, dy, a, flag);
 }
 
-// Axis-aligned box (xmin, -xmax, ymin, -ymax) of a point set, warp-reduced; lane 0 of
-// each warp stores its warp's box in s_box[warp].
-__device__ __forceinline__ void warp_box_store(double b0, double b1, double b2, double b3, int lane, double* s_box) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    b0 = fmin(b0, __shfl_xor_sync(0xffffffffu, b0, o));
-    b1 = fmin(b1, __shfl_xor_sync(0xffffffffu, b1, o));
-    b2 = fmin(b2, __shfl_xor_sync(0xffffffffu, b2, o));
-    b3 = fmin(b3, __shfl_xor_sync(0xffffffffu, b3, o));
-  }
-  if (lane == 0) {
-    s_box[0] = b0;
-    s_box[1] = b1;
-    s_box[2] = b2;
-    s_box[3] = b3;
-  }
-}
-
 // Images whose every (target, source) pair between the row box and the column box has
 // beta^2 r^2 >= xcut2 get their bit cleared: the per-pair test would skip all of them.
 // The box gap is a lower bound of |(t - s) - shift| per axis; the 1e-4 margin covers
@@ -368,17 +364,10 @@ template <int NXI, int NROW>
 __device__ __forceinline__ unsigned image_mask(const double* rb, const double* cb, const NearArgs& a) {
   unsigned mask = 0;
 #pragma unroll
-  for (int n = 0; n < NROW; ++n) {
-    const double ylo = (rb[2] + cb[3]) - a.shy[n];  // tymin - symax - shift
-    const double yhi = (-rb[3] - cb[2]) - a.shy[n];
-    const double gy = ylo > 0.0 ? ylo : (yhi < 0.0 ? -yhi : 0.0);
-#pragma unroll
-    for (int m = 0; m < NXI; ++m) {
-      const double xlo = (rb[0] + cb[1]) - a.shx[n * NXI + m];
-      const double xhi = (-rb[1] - cb[0]) - a.shx[n * NXI + m];
-      const double gx = xlo > 0.0 ? xlo : (xhi < 0.0 ? -xhi : 0.0);
-      if (a.beta2 * fma(gx, gx, gy * gy) * 0.9999 < a.xcut2) mask |= 1u << (n * NXI + m);
-    }
+  for (int img = 0; img < NXI * NROW; ++img) {
+    double lo, hi;
+    image_xrange(rb, cb, a.shx[img], a.shy[img / NXI], a.beta2, lo, hi);
+    if (lo * 0.9999 < a.xcut2) mask |= 1u << img;
   }
   return mask;
 }
@@ -478,8 +467,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     if constexpr (K::CULL) warp_box_store(cb[0], cb[1], cb[2], cb[3], lane, s_cbox[warp]);
     __syncthreads();
     unsigned mask = ~0u;
+    double rb[4], cbx[4];
     if (K::CULL && a.cull) {
-      double rb[4], cbx[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         rb[c] = fmin(fmin(s_rbox[0][c], s_rbox[1][c]), fmin(s_rbox[2][c], s_rbox[3][c]));
@@ -514,28 +503,47 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         if (!((mask >> img) & 1u)) continue;
         const double shx = a.shx[img], shy = a.shy[img / NXI];
         const bool ident = img == a.id_img;
+        int regime = 0;  // per-pair dispatch unless the boxes pin the whole tile pair
+        if (a.cull) {
+          double lo, hi;
+          image_xrange(rb, cbx, shx, shy, a.beta2, lo, hi);
+          regime = pwk::regime_of(lo, hi, a.xcut2);
+        }
+        auto sweep = [&](auto reg) {
+          constexpr int R = decltype(reg)::value;
 #pragma unroll 2
-        for (int i = 0; i < TILE; ++i) {
-          const int jj = (lane + i) & (TILE - 1);
-          const double sx = s_x[jj], sy = s_y[jj];
-          double w[K::NW];
+          for (int i = 0; i < TILE; ++i) {
+            const int jj = (lane + i) & (TILE - 1);
+            const double sx = s_x[jj], sy = s_y[jj];
+            double w[K::NW];
 #pragma unroll
-          for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
-          double cacc[K::NACC];
+            for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+            double cacc[K::NACC];
 #pragma unroll
-          for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+            for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
 #pragma unroll
-          for (int k = 0; k < TPT; ++k) {
-            double V[K::NV];
-            // (t - s) - shift as upstream (apply.cpp:534)
-            if (K::image_value(V, (tx[k] - sx) - shx, (ty[k] - sy) - shy, ident, a, flag)) {
+            for (int k = 0; k < TPT; ++k) {
+              double V[K::NV];
+              // (t - s) - shift as upstream (apply.cpp:534)
+              const double rx = (tx[k] - sx) - shx, ry = (ty[k] - sy) - shy;
+              if constexpr (R == 0) {
+                if (!K::image_value(V, rx, ry, ident, a, flag)) continue;
+              } else {
+                K::template image_fast<R == 2>(V, rx, ry, a);
+              }
               K::row(racc[k], V, w);
               K::col(cacc, V, tw[k]);
             }
-          }
 #pragma unroll
-          for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
-        }
+            for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+          }
+        };
+        if (regime == 2)
+          sweep(std::integral_constant<int, 2>{});
+        else if (regime == 1)
+          sweep(std::integral_constant<int, 1>{});
+        else
+          sweep(std::integral_constant<int, 0>{});
       }
       careful = false;
     }
