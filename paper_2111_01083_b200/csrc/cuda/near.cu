@@ -136,6 +136,13 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
     const double X = a.beta2 * r2;
     if (pwk::lt_hi(X, a.xcut2)) acc[0] = fma(w[0], pwk::k01_tile<LOWP, false>(X).k0, acc[0]);
   }
+  // the same for a pair known to be in asymptotic regime FAR and inside the cut-off
+  template <bool FAR>
+  __device__ __forceinline__ static void image_fast(double* acc, double rx, double ry, const double* w,
+                                                    const NearArgs& a) {
+    const double X = a.beta2 * fma(rx, rx, ry * ry);
+    acc[0] = fma(w[0], pwk::k01_asym<LOWP, false, FAR>(X).k0, acc[0]);
+  }
   __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
     out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
   }
@@ -191,6 +198,16 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
       acc[1] = fma(g, rx, acc[1]);
       acc[2] = fma(g, ry, acc[2]);
     }
+  }
+  template <bool FAR>
+  __device__ __forceinline__ static void image_fast(double* acc, double rx, double ry, const double* w,
+                                                    const NearArgs& a) {
+    const double X = a.beta2 * fma(rx, rx, ry * ry);
+    const pwk::K01 k = pwk::k01_asym<LOWP, true, FAR>(X);
+    acc[0] = fma(w[0], k.k0, acc[0]);
+    const double g = w[0] * k.k1_over_x;
+    acc[1] = fma(g, rx, acc[1]);
+    acc[2] = fma(g, ry, acc[2]);
   }
   __device__ __forceinline__ static void finish(const double* acc, const NearArgs& a, double* out) {
     out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
@@ -450,6 +467,24 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
   int flag = 0;
   const typename HasConsts<KER>::type C = HasConsts<KER>::make();
   if constexpr (UsesExpTab<KER>::value) pwk::exp_tab_fill();  // visible after the tile loop's first __syncthreads
+  // screened kernels: bounding boxes of the block's targets and of each source tile give
+  // per-image masks and regimes (binned inputs make both compact; near_sym_impl.cuh)
+  constexpr bool kBoxes = ImageOuter<KER>::value;
+  constexpr int kWarpsT = kThreads / 32;
+  __shared__ double s_tbox[kBoxes ? kWarpsT : 1][4], s_sbox[kBoxes ? kWarpsT : 1][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (kBoxes) {
+    double b[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#pragma unroll
+    for (int k = 0; k < TPT; ++k)
+      if (live[k]) {
+        b[0] = fmin(b[0], tx[k]);
+        b[1] = fmin(b[1], -tx[k]);
+        b[2] = fmin(b[2], ty[k]);
+        b[3] = fmin(b[3], -ty[k]);
+      }
+    warp_box_store(b[0], b[1], b[2], b[3], lane, s_tbox[warp]);  // read after the loop's syncs
+  }
 
   const size_t j_begin = static_cast<size_t>(blockIdx.y) * a.src_per_split;
   size_t j_end = j_begin + a.src_per_split;
@@ -458,10 +493,17 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
   for (size_t j0 = j_begin; j0 < j_end; j0 += kTile) {
     const int tn = static_cast<int>((j_end - j0) < kTile ? (j_end - j0) : kTile);
     __syncthreads();
+    double sb[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     for (int i = threadIdx.x; i < tn; i += kThreads) {
       const double2 p = a.src[j0 + i];
       s_x[i] = p.x;
       s_y[i] = p.y;
+      if (kBoxes) {
+        sb[0] = fmin(sb[0], p.x);
+        sb[1] = fmin(sb[1], -p.x);
+        sb[2] = fmin(sb[2], p.y);
+        sb[3] = fmin(sb[3], -p.y);
+      }
       if (KER::NW == 1) {
         s_w[0][i] = a.q[j0 + i];
       } else {
@@ -475,24 +517,51 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
         }
       }
     }
+    if constexpr (kBoxes) warp_box_store(sb[0], sb[1], sb[2], sb[3], lane, s_sbox[warp]);
     __syncthreads();
     if constexpr (ImageOuter<KER>::value) {
       // screened kernels: image-outer order (loop-invariant shift, one K0 per inner
-      // iteration, small code; near_sym_impl.cuh does the same on its off-diagonal tiles)
+      // iteration, small code; near_sym_impl.cuh does the same on its off-diagonal tiles);
+      // an image whose box range lies beyond the cut-off is skipped, one whose range lies in
+      // one asymptotic regime runs branch-free (same arithmetic as the per-pair dispatch)
+      double tb[4], sbx[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        tb[c] = fmin(fmin(s_tbox[0][c], s_tbox[1][c]), fmin(s_tbox[2][c], s_tbox[3][c]));
+        sbx[c] = fmin(fmin(s_sbox[0][c], s_sbox[1][c]), fmin(s_sbox[2][c], s_sbox[3][c]));
+      }
 #pragma unroll 1
       for (int img = 0; img < NXI * NROW; ++img) {
         const double shx = a.shx[img], shy = a.shy[img / NXI];
         const bool ident = img == a.id_img;
+        double lo, hi;
+        image_xrange(tb, sbx, shx, shy, a.beta2, lo, hi);
+        if (a.cull && lo * 0.9999 >= a.xcut2) continue;  // block-uniform
+        const int regime = a.cull ? pwk::regime_of(lo, hi, a.xcut2) : 0;
+        auto sweep = [&](auto reg) {
+          constexpr int R = decltype(reg)::value;
 #pragma unroll 2
-        for (int i = 0; i < tn; ++i) {
-          const double sx = s_x[i], sy = s_y[i];
-          double w[KER::NW];
+          for (int i = 0; i < tn; ++i) {
+            const double sx = s_x[i], sy = s_y[i];
+            double w[KER::NW];
 #pragma unroll
-          for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
+            for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
 #pragma unroll
-          for (int k = 0; k < TPT; ++k)  // (t - s) - shift, the reference's association (apply.cpp:534)
-            KER::image(acc[k], (tx[k] - sx) - shx, (ty[k] - sy) - shy, w, ident, a, flag);
-        }
+            for (int k = 0; k < TPT; ++k) {  // (t - s) - shift, the reference's association (apply.cpp:534)
+              const double rx = (tx[k] - sx) - shx, ry = (ty[k] - sy) - shy;
+              if constexpr (R == 0)
+                KER::image(acc[k], rx, ry, w, ident, a, flag);
+              else
+                KER::template image_fast<R == 2>(acc[k], rx, ry, w, a);
+            }
+          }
+        };
+        if (regime == 2)
+          sweep(std::integral_constant<int, 2>{});
+        else if (regime == 1)
+          sweep(std::integral_constant<int, 1>{});
+        else
+          sweep(std::integral_constant<int, 0>{});
       }
       continue;
     }

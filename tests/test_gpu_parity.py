@@ -353,19 +353,24 @@ def test_symmetric_targets_equal_sources(pw, gpu, ref, name, n):
     assert rel_l2(sym[idx], want, gauge) <= 10 * c.eps
 
 
+@pytest.mark.parametrize("sym", [True, False])
 @pytest.mark.parametrize("grad", [False, True])
-def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad):
-    """The screened symmetric tile drops, per tile pair, the images whose bounding-box gap
-    puts every pair beyond the K0 cut-off (near_sym_impl.cuh image_mask). The per-pair test
-    would skip those pairs anyway, so the fixed-point sums are bitwise those without the
-    mask (PWB_NO_CULL=1). Wide cell (c5's aspect) so most tile pairs lose images."""
+@pytest.mark.parametrize("cellt,beta", [((100.0, 0.0, 1.0, 2), 1.0), ((1.0, 0.3, 0.8, 2), 10.0)])
+def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad, sym, cellt, beta):
+    """The screened tiles drop, per tile pair, the images whose bounding-box gap puts every
+    pair beyond the K0 cut-off, and run a tile pair whose box range lies in one asymptotic
+    regime without the per-pair dispatch (near_sym_impl.cuh, near.cu; pw_math.cuh
+    regime_of). Both give the per-pair path's values, so the results are bitwise those
+    with PWB_NO_CULL=1. Symmetric and one-sided tiles; c5's wide cell (most tile pairs lose
+    images) and c2's skewed cell at beta = 10 (regimes near and far mixed)."""
     rng = np.random.default_rng(123)
     n = 40000
-    cellt = (100.0, 0.0, 1.0, 2)
-    src = np.ascontiguousarray(np.column_stack([rng.uniform(-50, 50, n), rng.uniform(-0.5, 0.5, n)]))
+    d, xi, eta = cellt[:3]
+    u = rng.uniform(-0.5, 0.5, (n, 2))
+    src = np.ascontiguousarray(np.column_stack([u[:, 0] * d + u[:, 1] * xi, u[:, 1] * eta]))
     q = np.ascontiguousarray(rng.standard_normal(n))
-    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, _cell(pw, cellt), 1e-8)
-    s = pw.ParticleSystem(sources=src, targets=src, charges=q)
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, beta, _cell(pw, cellt), 1e-8)
+    s = pw.ParticleSystem(sources=src, targets=src if sym else src.copy(), charges=q)
     culled = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
     monkeypatch.setenv("PWB_NO_CULL", "1")
     full = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
