@@ -28,12 +28,16 @@
 #ifndef PWB_MH_UNROLL_M
 #define PWB_MH_UNROLL_M 3  // image columns per unrolled step (screened kernels; c2: 1 -> 929 ms, 2 -> 807, 3 -> 792, 5 -> 890)
 #endif
+#ifndef PWB_MH_SRC_UNROLL
+#define PWB_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c2: 2 -> 579 ms, 4 -> 566)
+#endif
 #ifndef PWB_MH_TPT
 #define PWB_MH_TPT 1  // targets per thread of the screened one-sided tiles
 #endif
 namespace pwb {
 namespace {
 constexpr int kMhUnrollM = PWB_MH_UNROLL_M;
+constexpr int kMhSrcUnroll = PWB_MH_SRC_UNROLL;
 }
 }  // namespace pwb
 
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
         const int regime = a.cull ? pwk::regime_of(lo, hi, a.xcut2) : 0;
         auto sweep = [&](auto reg) {
           constexpr int R = decltype(reg)::value;
-#pragma unroll 2
+#pragma unroll kMhSrcUnroll
           for (int i = 0; i < tn; ++i) {
             const double sx = s_x[i], sy = s_y[i];
             double w[KER::NW];

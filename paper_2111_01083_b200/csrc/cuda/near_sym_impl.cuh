@@ -50,6 +50,12 @@ namespace sym {
 #ifndef PWB_SYM_MH_UNROLL_M
 #define PWB_SYM_MH_UNROLL_M 3  // image columns per unrolled step of the screened symmetric tile (c5 slice: 1 -> 573 ms, 3 -> 480)
 #endif
+#ifndef PWB_SYM_MH_SRC_UNROLL
+#define PWB_SYM_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c5 slice: 2 -> 159 ms, 4 -> 154)
+#endif
+#ifndef PWB_SYM_MH_TPT
+#define PWB_SYM_MH_TPT 2  // targets per thread of the screened symmetric tile
+#endif
 #ifndef PWB_SYM_LAPLACE_UNROLL
 #define PWB_SYM_LAPLACE_UNROLL 4  // sources per unrolled step of the fast loop (c4: 904 -> 895 ms vs 2)
 #endif
@@ -61,6 +67,7 @@ namespace sym {
 #endif
 constexpr int kT = 128;  // threads per block
 constexpr int kSymMhUnrollM = PWB_SYM_MH_UNROLL_M;
+constexpr int kSymMhSrcUnroll = PWB_SYM_MH_SRC_UNROLL;
 constexpr int kWarps = kT / 32;
 
 // ---------------------------------------------------------------- fixed point
@@ -137,7 +144,8 @@ struct SymLaplace {
 
 template <bool GRAD, bool LOWP_>
 struct SymModHelm {
-  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = 2, CHUNK = 16, MINB = 0, UNROLL = 1;
+  static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = PWB_SYM_MH_TPT, CHUNK = 16, MINB = 0,
+                       UNROLL = 1;
   static constexpr bool FAST = false, LOWP = LOWP_;
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
@@ -511,7 +519,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         }
         auto sweep = [&](auto reg) {
           constexpr int R = decltype(reg)::value;
-#pragma unroll 2
+#pragma unroll kSymMhSrcUnroll
           for (int i = 0; i < TILE; ++i) {
             const int jj = (lane + i) & (TILE - 1);
             const double sx = s_x[jj], sy = s_y[jj];
