@@ -210,6 +210,14 @@ int pwb_far_target_pass(const pwb_periodizer* pz, const pwb_system* sys, const p
 int pwb_near_sym_items(const pwb_periodizer* pz, size_t n, const pwb_options* opt, long* n_items, int* nout);
 int pwb_near_sym_partial(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, long item_begin,
                          long item_end, int64_t* acc);
+/* Item boundaries bounds[0..world] (host array of world + 1, world <= 64) of a balanced split of
+ * the symmetric work items over `world` ranks: rank r runs [bounds[r], bounds[r+1]). For the
+ * screened kernels (modified Helmholtz) the split balances the estimated cost per item from
+ * the tile bounding boxes (their image masks and regimes make item costs differ); for the
+ * others it is the even split by count. Same inputs give the same bounds on every rank.
+ * Extension (multi-GPU; no reference counterpart). */
+int pwb_near_sym_split(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, int world,
+                       long* bounds);
 int pwb_fixed_to_field(const pwb_periodizer* pz, const pwb_options* opt, const int64_t* acc, size_t n_targets,
                        pwb_field* out);
 /* Strength/neutrality/cell checks of apply_far (proj/src/apply.cpp:350-393, cell.cpp:77-94),

@@ -133,8 +133,8 @@ EXPORTED = [
     "pwb_far_coeff_size", "pwb_far_source_pass", "pwb_far_target_pass", "pwb_validate",
     "pwb_nufft_type1", "pwb_nufft_type2", "pwb_nufft_type3", "pwb_fast_nufft_available",
     "pwb_eval_kernel", "pwb_rng_uniform", "pwb_launch_count", "pwb_last_phase_ms", "pwb_fp64_peak_probe",
-    "pwb_near_sym_items", "pwb_near_sym_partial", "pwb_fixed_to_field", "pwb_brute_force_far",
-    "pwb_periodicity_residual",
+    "pwb_near_sym_items", "pwb_near_sym_partial", "pwb_near_sym_split", "pwb_fixed_to_field",
+    "pwb_brute_force_far", "pwb_periodicity_residual",
 ]
 
 _lib = None
@@ -190,6 +190,8 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(i)]
     L.pwb_near_sym_partial.argtypes = [vp, ctypes.POINTER(_System), ctypes.POINTER(_Options), ctypes.c_long,
                                        ctypes.c_long, vp]
+    L.pwb_near_sym_split.argtypes = [vp, ctypes.POINTER(_System), ctypes.POINTER(_Options), i,
+                                     ctypes.POINTER(ctypes.c_long)]
     L.pwb_fixed_to_field.argtypes = [vp, ctypes.POINTER(_Options), vp, sz, ctypes.POINTER(_Field)]
     L.pwb_brute_force_far.argtypes = [vp, ctypes.POINTER(_System), i, ctypes.POINTER(_Options),
                                       ctypes.POINTER(_Field)]
@@ -681,6 +683,18 @@ def near_sym_partial(pz: Periodizer, sys: ParticleSystem, acc, item_begin: int, 
                                       acc.data_ptr()))
 
 
+def near_sym_split(pz: Periodizer, sys: ParticleSystem, world: int, opt: Optional[ApplyOptions] = None):
+    """Item boundaries (world + 1 ints) of a balanced split of the symmetric work items
+    (pwb_near_sym_split: cost-balanced for the screened kernels, by count otherwise)."""
+    s, mem = sys._c()
+    if mem != MEM_DEVICE:
+        raise ValueError("near_sym_split takes device tensors")
+    b = (ctypes.c_long * (world + 1))()
+    o = (opt or ApplyOptions())._c()
+    _check(lib().pwb_near_sym_split(pz.handle, ctypes.byref(s), ctypes.byref(o), int(world), b))
+    return [int(v) for v in b]
+
+
 def fixed_to_field(pz: Periodizer, acc, n_targets: int, out: FieldResult, opt: Optional[ApplyOptions] = None,
                    like=None) -> FieldResult:
     """out += the fp64 value of a fixed-point accumulator slice (device)."""
@@ -697,5 +711,6 @@ __all__ = [
     "make_stokes_dlp_periodizer", "make_multipole_periodizer", "ParticleSystem", "ApplyOptions", "FieldResult",
     "total_field", "apply_far", "accumulate", "near_field", "choose_path", "fast_nufft_available", "nufft_type1",
     "nufft_type2", "nufft_type3", "eval_kernel", "far_coeff_size", "far_source_pass", "far_target_pass",
+    "near_sym_split",
     "device_count", "lib", "EXPORTED",
 ]

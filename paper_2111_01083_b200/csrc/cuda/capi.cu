@@ -751,6 +751,22 @@ int pwb_near_sym_partial(const pwb_periodizer* h, const pwb_system* s, const pwb
   });
 }
 
+int pwb_near_sym_split(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, int world,
+                       long* bounds) {
+  if (!h || !s || !bounds) return fail_arg("null argument");
+  if (s->memory != PWB_MEM_DEVICE) return fail_arg("sharded passes take device memory");
+  return guard([&] {
+    const int dev = current_device(o ? o->device : -1);
+    pwb::Plan& p = const_cast<pwb_periodizer*>(h)->plan(dev);
+    std::lock_guard<std::mutex> lock(p.mutex());
+    pwb::Opts opt = opts_from(o);
+    pwb::DevSys ds;
+    stage_in(p, s, p.stream_for(opt), &ds);
+    p.sym_split(ds, opt, world, bounds);
+    return OK;
+  });
+}
+
 int pwb_fixed_to_field(const pwb_periodizer* h, const pwb_options* o, const int64_t* acc, size_t n, pwb_field* f) {
   if (!h || !acc || !f) return fail_arg("null argument");
   if (f->memory != PWB_MEM_DEVICE) return fail_arg("fixed-point conversion takes device memory");

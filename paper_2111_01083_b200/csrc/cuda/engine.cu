@@ -948,6 +948,34 @@ long Plan::sym_items(const Opts& o, size_t n) {
   return near_sym_item_count(nk, n);
 }
 
+// Screened kernels (binned, masked, regime sweeps) cost very different amounts per work
+// item -- c5's far tile pairs lose most images -- so their items are split by estimated
+// cost (near_sym.cu near_sym_split; every rank computes the same bounds from the same
+// points); the other kernels' items cost the same, split by count.
+void Plan::sym_split(const DevSys& s, const Opts& o, int world, long* bounds) {
+  require(world >= 1 && world <= 64, ErrorCode::Unsupported, "world size must be in [1, 64]");
+  NearArgs a;
+  const NearKind nk = near_args(s, o, DevOut{}, false, 0, 0, false, a);
+  const long items = near_sym_supported(nk) ? near_sym_item_count(nk, s.nt) : 0;
+  const bool screened = near_screened(nk, a) && s.nt >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr &&
+                        std::getenv("PWB_COUNT_SPLIT") == nullptr;
+  if (!screened || world == 1 || items == 0) {
+    for (int r = 0; r <= world; ++r) bounds[r] = items * r / world;
+    return;
+  }
+  require(s.tgt == s.src && s.nt == s.ns, ErrorCode::Unsupported, "the symmetric near field needs the sources as targets");
+  cudaStream_t st = stream_for(o);
+  bin_inputs(s, a, st);  // the same sorted points sym_partial runs on
+  const size_t nb = near_sym_tiles(s.nt);
+  int* rs_dev = sym_rows_.as<int>(nb + 1);
+  int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
+  const size_t bytes = near_sym_split_bytes(s.nt, items);
+  void* ws = sym_split_ws_.ensure(bytes);
+  long* hb = static_cast<long*>(host_checks_.ensure(65 * sizeof(long)));
+  near_sym_split(nk, a, world, hb, ws, bytes, rs_dev, rs_host, st);
+  for (int r = 0; r <= world; ++r) bounds[r] = hb[r];
+}
+
 int Plan::near_nout(const Opts& o) const {
   NearArgs a;
   return static_cast<int>(near_outputs(near_args(DevSys{}, o, DevOut{}, false, 0, 0, false, a)));

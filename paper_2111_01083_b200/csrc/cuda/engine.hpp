@@ -160,6 +160,8 @@ class Plan {
   long sym_items(const Opts& o, size_t n);
   int near_nout(const Opts& o) const;
   void sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc);
+  // item boundaries [world + 1] of a balanced multi-GPU split of the symmetric items
+  void sym_split(const DevSys& s, const Opts& o, int world, long* bounds);
   void fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, const DevOut& out);
   // full pipeline on device pointers; returns the accelerated flag
   bool total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images);
@@ -180,7 +182,7 @@ class Plan {
   std::vector<std::unique_ptr<Family>> fams_;
   DevBuf s2pw_partial_, coeff_ws_, A_, B_, m0_, near_partial_, flag_, red_m_, red_c_, red_out_;
   PinnedBuf host_checks_;
-  DevBuf sym_fx_, sym_rows_;
+  DevBuf sym_fx_, sym_rows_, sym_split_ws_;
   PinnedBuf sym_rows_host_;
   // spatially binned copies of the near-field inputs (binning.cu)
   DevBuf bin_ws_, bin_perm_s_, bin_perm_t_, bin_src_, bin_tgt_, bin_q_, bin_vec_, bin_nrm_;

@@ -4,6 +4,8 @@
 // near_sym_modhelm.cu and near_sym_stokes.cu.
 #include "near_sym_impl.cuh"
 
+#include <cub/device/device_scan.cuh>
+
 namespace pwb {
 namespace {
 
@@ -46,7 +48,152 @@ long item_count(size_t n) {
   for (long I = 0; I < nb; ++I) items += (nb - I + K::CHUNK - 1) / K::CHUNK;
   return items;
 }
+// ---- cost-balanced item ranges for the multi-GPU split of the screened tiles ----------
+// Bounding box (xmin, -xmax, ymin, -ymax) of every tile; one warp per tile.
+__global__ void tile_box_kernel(const double2* __restrict__ p, size_t n, int tile, int nb, double* __restrict__ box) {
+  const int t = static_cast<int>((static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= nb) return;
+  double b[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  const size_t j0 = static_cast<size_t>(t) * tile;
+  for (int i = lane; i < tile; i += 32) {
+    const size_t j = j0 + i;
+    if (j >= n) break;
+    const double2 q = p[j];
+    b[0] = fmin(b[0], q.x);
+    b[1] = fmin(b[1], -q.x);
+    b[2] = fmin(b[2], q.y);
+    b[3] = fmin(b[3], -q.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) b[c] = fmin(b[c], __shfl_xor_sync(0xffffffffu, b[c], o));
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) box[4 * static_cast<size_t>(t) + c] = b[c];
+}
+
+// Estimated cost of every work item (row tile I, column tiles J0..J1): per tile pair a
+// staging overhead plus, per image, what the tile will do with it (near_sym_impl.cuh):
+// nothing when masked, a branch-free regime sweep, or the per-pair dispatch.
+__global__ void item_cost_kernel(const double* __restrict__ box, const int* __restrict__ row_start, int nb, int chunk,
+                                 long items, const NearArgs a, float* __restrict__ cost) {
+  const long item = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= items) return;
+  int lo = 0, hi = nb;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (row_start[mid] <= item)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int I = lo;
+  const int J0 = I + static_cast<int>(item - row_start[I]) * chunk;
+  const int J1 = min(nb, J0 + chunk);
+  double rb[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) rb[c] = box[4 * static_cast<size_t>(I) + c];
+  float c_item = 0.0f;
+  for (int J = J0; J < J1; ++J) {
+    double cb[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cb[c] = box[4 * static_cast<size_t>(J) + c];
+    float c_pair = 0.25f;  // staging, boxes, column flush
+    for (int img = 0; img < a.nxi * a.nrow; ++img) {
+      double xl, xh;
+      image_xrange(rb, cb, a.shx[img], a.shy[img / a.nxi], a.beta2, xl, xh);
+      if (xl * 0.9999 >= a.xcut2) continue;
+      c_pair += J == I ? 2.0f : (pwk::regime_of(xl, xh, a.xcut2) ? 1.0f : 1.4f);
+    }
+    c_item += c_pair;
+  }
+  cost[item] = c_item;
+}
+
+// bounds[r] = first item whose inclusive cost prefix exceeds r / world of the total
+__global__ void split_kernel(const float* __restrict__ prefix, long items, int world, long* __restrict__ bounds) {
+  const int r = threadIdx.x;
+  if (r > world) return;
+  if (r == 0 || r == world) {
+    bounds[r] = r == 0 ? 0 : items;
+    return;
+  }
+  const double target = static_cast<double>(prefix[items - 1]) * r / world;
+  long lo = 0, hi = items;  // first index with prefix > target
+  while (lo < hi) {
+    const long mid = (lo + hi) >> 1;
+    if (static_cast<double>(prefix[mid]) > target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  bounds[r] = lo;
+}
+
 }  // namespace
+
+void near_sym_shape(NearKind kind, int* tile, int* chunk) {
+  auto set = [&](auto k) {
+    using K = decltype(k);
+    *tile = sym::kT * K::TPT;
+    *chunk = K::CHUNK;
+  };
+  switch (kind) {
+    case NearKind::Laplace: set(sym::SymLaplace<false>{}); break;
+    case NearKind::ModHelm: set(sym::SymModHelm<false, false>{}); break;
+    case NearKind::ModHelmGrad: set(sym::SymModHelm<true, false>{}); break;
+    case NearKind::Stokes: set(sym::SymStokes<false, false>{}); break;
+    case NearKind::StokesP: set(sym::SymStokes<true, false>{}); break;
+    default: *tile = 0; *chunk = 0;
+  }
+}
+
+size_t near_sym_split_bytes(size_t n, long items) {
+  size_t tmp = 0;
+  cuda_check(cub::DeviceScan::InclusiveSum(nullptr, tmp, static_cast<const float*>(nullptr), static_cast<float*>(nullptr),
+                                           static_cast<int>(items > 0 ? items : 1)),
+             "scan size");
+  const size_t nb = near_sym_tiles(n);
+  return 4 * nb * sizeof(double) + 2 * static_cast<size_t>(items) * sizeof(float) + tmp + 65 * sizeof(long) + 6 * 256;
+}
+
+void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_host, void* ws, size_t ws_bytes,
+                    int* row_start_dev, int* row_start_host, cudaStream_t st) {
+  int tile = 0, chunk = 0;
+  near_sym_shape(kind, &tile, &chunk);
+  const int nb = static_cast<int>((a.nt + tile - 1) / tile);
+  long items = 0;
+  for (int I = 0; I < nb; ++I) {
+    row_start_host[I] = static_cast<int>(items);
+    items += (nb - I + chunk - 1) / chunk;
+  }
+  row_start_host[nb] = static_cast<int>(items);
+  auto align = [](size_t v) { return (v + 255) & ~static_cast<size_t>(255); };
+  char* base = static_cast<char*>(ws);
+  double* box = reinterpret_cast<double*>(base);
+  size_t off = align(4 * static_cast<size_t>(nb) * sizeof(double));
+  float* cost = reinterpret_cast<float*>(base + off);
+  off += align(static_cast<size_t>(items) * sizeof(float));
+  float* prefix = reinterpret_cast<float*>(base + off);
+  off += align(static_cast<size_t>(items) * sizeof(float));
+  long* bounds = reinterpret_cast<long*>(base + off);
+  off += align(65 * sizeof(long));
+  if (off > ws_bytes || world > 64) throw_internal("near_sym_split: workspace");
+  size_t tmp = ws_bytes - off;
+  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+             "row starts");
+  tile_box_kernel<<<static_cast<unsigned>((static_cast<size_t>(nb) * 32 + 255) / 256), 256, 0, st>>>(a.tgt, a.nt, tile,
+                                                                                                    nb, box);
+  item_cost_kernel<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(box, row_start_dev, nb, chunk, items,
+                                                                                a, cost);
+  cuda_check(cub::DeviceScan::InclusiveSum(base + off, tmp, cost, prefix, static_cast<int>(items), st), "scan");
+  split_kernel<<<1, 128, 0, st>>>(prefix, items, world, bounds);
+  count_launches(3);
+  cuda_check(cudaMemcpyAsync(bounds_host, bounds, (world + 1) * sizeof(long), cudaMemcpyDeviceToHost, st), "D2H bounds");
+  cuda_check(cudaStreamSynchronize(st), "split sync");
+}
 
 long near_sym_item_count(NearKind kind, size_t n) {
   switch (kind) {

@@ -93,6 +93,13 @@ void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int 
                       cudaStream_t st);
 // host-only: number of work items of the symmetric decomposition (0 if none)
 long near_sym_item_count(NearKind kind, size_t n);
+// Tile size (points) and column tiles per work item of the symmetric tile of `kind`.
+void near_sym_shape(NearKind kind, int* tile, int* chunk);
+// Cost-balanced item boundaries (world + 1 longs, host) for the screened symmetric tiles:
+// tile boxes of the (binned) points in a.tgt, estimated item costs, prefix sum, split.
+size_t near_sym_split_bytes(size_t n, long items);
+void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_host, void* ws, size_t ws_bytes,
+                    int* row_start_dev, int* row_start_host, cudaStream_t st);
 
 // ---------------------------------------------------------------- far field (direct S2PW / PW2T)
 // Weight sets: what each source contributes per mode (K real weights).

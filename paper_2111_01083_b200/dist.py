@@ -96,7 +96,14 @@ def sharded_total_field(backend, comm: Comm, plan: ShardPlan, symmetric: bool):
     out = backend.far_target(coeff, t_lo, t_hi)
     if symmetric:
         items, nout = backend.near_items()
-        i_lo, i_hi = contiguous(items, plan.world, plan.rank)
+        # balanced item ranges: by estimated cost for the screened kernels (identical on
+        # every rank: the same points give the same bounds), by count otherwise
+        split = getattr(backend, "near_split", None)
+        if split is not None:
+            bounds = split(plan.world)
+            i_lo, i_hi = bounds[plan.rank], bounds[plan.rank + 1]
+        else:
+            i_lo, i_hi = contiguous(items, plan.world, plan.rank)
         acc = backend.accumulator(plan.chunk * plan.world * nout * 3)
         backend.near_partial(i_lo, i_hi, acc)
         mine = backend.accumulator(plan.chunk * nout * 3)
@@ -141,6 +148,10 @@ class CudaBackend:
     def near_partial(self, lo, hi, acc):
         sys_ = self.pw.ParticleSystem(sources=self.src, targets=self.src, **{self.kw: self.q})
         self.pw.near_sym_partial(self.pz, sys_, acc, lo, hi, self.opt)
+
+    def near_split(self, world):
+        sys_ = self.pw.ParticleSystem(sources=self.src, targets=self.src, **{self.kw: self.q})
+        return self.pw.near_sym_split(self.pz, sys_, world, self.opt)
 
     def fixed_to_out(self, acc, n, out):
         ref = out.scalar if out.scalar is not None else out.velocity

@@ -49,6 +49,42 @@ def test_symmetric_items_compose_bitwise(pw, gpu, monkeypatch, name, n, pressure
             assert torch.equal(got.pressure, whole.pressure)
 
 
+@pytest.mark.parametrize("name,n", [("c5", 60000), ("c4", 40000)])
+def test_balanced_split_covers_items_and_composes(pw, gpu, name, n):
+    """pwb_near_sym_split: monotone bounds from 0 to the item count, identical on repeated
+    calls (every rank must compute the same split), and the per-rank partials over those
+    ranges add up bitwise to the single call. Screened kernels (c5) split by estimated cost,
+    the others (c4) by count."""
+    import torch
+
+    from paper_2111_01083_b200 import configs
+
+    inp = configs.generate(name, n_src=n)
+    c = inp.config
+    pz = pw.make_periodizer(c.pde, c.beta, pw.make_unit_cell(*c.cell[:3], c.cell[3]), c.eps)
+    src = torch.from_numpy(inp.sources).cuda()
+    q = torch.from_numpy(inp.charges).cuda()
+    opt = pw.ApplyOptions()
+    s = pw.ParticleSystem(sources=src, targets=src, charges=q)
+    items, nout = pw.near_sym_items(pz, n, opt)
+    whole = pw.near_field(pz, s, opt)
+    for world in (3, 8):
+        b = pw.near_sym_split(pz, s, world, opt)
+        assert b == pw.near_sym_split(pz, s, world, opt)
+        assert b[0] == 0 and b[-1] == items and all(x <= y for x, y in zip(b, b[1:]))
+        if name == "c4":
+            assert b == [items * r // world for r in range(world + 1)]
+        acc = torch.zeros(n * nout * 3, dtype=torch.int64, device="cuda")
+        for r in range(world):
+            part = torch.zeros_like(acc)
+            pw.near_sym_partial(pz, s, part, b[r], b[r + 1], opt)
+            acc += part
+        got = pw.FieldResult()
+        got.scalar = torch.zeros_like(whole.scalar)
+        pw.fixed_to_field(pz, acc, n, got, opt, like=src)
+        assert torch.equal(got.scalar, whole.scalar)
+
+
 def test_sharded_total_field_matches_single_call(pw, gpu):
     """dist.sharded_total_field with a single-process Comm per simulated rank; the
     all-reduce / reduce-scatter are done by summing the per-rank buffers here."""
