@@ -105,7 +105,18 @@ __global__ void item_cost_kernel(const double* __restrict__ box, const int* __re
       double xl, xh;
       image_xrange(rb, cb, a.shx[img], a.shy[img / a.nxi], a.beta2, xl, xh);
       if (xl * 0.9999 >= a.xcut2) continue;
-      c_pair += J == I ? 2.0f : (pwk::regime_of(xl, xh, a.xcut2) ? 1.0f : 1.4f);
+      // relative costs calibrated on c5 at N = 1e6 (tools/shard_balance.py, 8 ranks:
+      // max/mean 1.14 -> 1.09 -> 1.04 -> 1.025 over three settings): a branch-free regime
+      // sweep 1, the per-pair dispatch 3.6 (regime-divergent warps, no cross-source
+      // interleave; all-series 3.0), the diagonal tile's careful image-inner path 7
+      float ci;
+      if (J == I)
+        ci = 7.0f;
+      else if (const int reg = pwk::regime_of(xl, xh, a.xcut2))
+        ci = reg == 2 ? 1.0f : 1.1f;
+      else
+        ci = xh * 1.0001 < 4.0 ? 3.0f : 3.6f;
+      c_pair += ci;
     }
     c_item += c_pair;
   }
