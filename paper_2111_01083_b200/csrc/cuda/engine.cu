@@ -897,6 +897,7 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
         for (int m = -c.m0; m <= c.m0; ++m) a.shx[(n + 1) * a.nxi + (m + c.m0)] = m * c.d + n * c.xi;
       }
       a.id_img = 1 * a.nxi + c.m0;
+      a.unskewed = c.xi == 0.0 ? 1 : 0;
     } else {
       a.nxi = 3;
       a.nrow = 1;

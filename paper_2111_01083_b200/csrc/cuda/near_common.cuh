@@ -15,9 +15,13 @@ __device__ __forceinline__ double row_dy(double dy, const NearArgs& a, int n) {
   if (fused && n == NROW / 2) return dy;
   return dy - a.shy[n];
 }
-template <int NXI, int NROW>
+// USK (unskewed cell, xi == 0): shx[n][m] = m d + n * 0.0 = m d for every row n, so every
+// row reads the middle row's shift -- the same value -- and the compiler forms each column's
+// rx once per pair instead of once per image (bitwise the same numbers).
+template <int NXI, int NROW, bool USK = false>
 __device__ __forceinline__ double img_dx(double dx, const NearArgs& a, int n, int m) {
   constexpr bool fused = !(NXI == 1 && NROW == 1);
+  if (USK) n = NROW / 2;
   if (fused && n == NROW / 2 && m == NXI / 2) return dx;
   return dx - a.shx[n * NXI + m];
 }

@@ -97,7 +97,7 @@ struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT, CHUNK = 8,
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
-  template <int NXI, int NROW, class LK, class B>
+  template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
     double ry2[NROW];
@@ -111,7 +111,7 @@ struct SymLaplace {
     for (int n = 0; n < NROW; ++n)
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double rx = img_dx<NXI, NROW, USK>(dx, a, n, m);
         P *= fma(rx, rx, ry2[n]);
       }
     V[0] = pwk::log_fast(P, K, bad);
@@ -149,7 +149,7 @@ struct SymModHelm {
   static constexpr bool FAST = false, LOWP = LOWP_;
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
-  template <int NXI, int NROW, class LK, class B>
+  template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
   // mask: bit n * NXI + m set for the images that may hold a pair with beta r < 64 in this
   // tile pair (block-uniform, so the skips are uniform branches)
@@ -250,7 +250,7 @@ struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
                        CHUNK = 16, MINB = 0, UNROLL = 2;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
-  template <int NXI, int NROW, class LK, class B>
+  template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
     double P = 1.0, txx = 0.0, txy = 0.0, px = 0.0, py = 0.0;
@@ -260,7 +260,7 @@ struct SymStokes {
       const double ry2 = ry * ry;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double rx = img_dx<NXI, NROW, USK>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
         const double inv = pwk::rcp_tier<LOWP>(r2);
@@ -380,7 +380,7 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
   return mask;
 }
 
-template <class K, int NXI, int NROW>
+template <class K, int NXI, int NROW, bool USK>
 __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   constexpr int TPT = K::TPT;
   constexpr int TILE = kT * TPT;
@@ -576,7 +576,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         for (int k = 0; k < TPT; ++k) {
           double V[K::NV];
           // (t - s) - shift as upstream (apply.cpp:534)
-          K::template values_fast<NXI, NROW>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
+          K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
           K::row(racc[k], V, w);
           K::col(cacc, V, tw[k]);
         }
@@ -654,18 +654,18 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 // K::MINB > 0 caps registers for K::MINB resident blocks per SM (one image row; the 2-D
 // image blocks hold more live shifts and get at most 4 -- 80 or 96 regs spill there).
 // MINB == 0 keeps ptxas's own allocation (the wider functors).
-template <class K, int NXI, int NROW>
+template <class K, int NXI, int NROW, bool USK>
 __global__ void __launch_bounds__(kT, NROW == 1 ? K::MINB : (K::MINB < 4 ? K::MINB : 4))
     near_sym_kernel_capped(const __grid_constant__ SymArgs S) {
-  near_sym_body<K, NXI, NROW>(S);
+  near_sym_body<K, NXI, NROW, USK>(S);
 }
 
-template <class K, int NXI, int NROW>
+template <class K, int NXI, int NROW, bool USK>
 __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
-  near_sym_body<K, NXI, NROW>(S);
+  near_sym_body<K, NXI, NROW, USK>(S);
 }
 
-template <class K, int NXI, int NROW>
+template <class K, int NXI, int NROW, bool USK = false>
 void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
                       int* row_start_host, const SymRange& range) {
   constexpr int TILE = kT * K::TPT;
@@ -699,9 +699,9 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
     static bool carveout = false;
     void (*kern)(const SymArgs);
     if constexpr (K::MINB > 0)
-      kern = near_sym_kernel_capped<K, NXI, NROW>;
+      kern = near_sym_kernel_capped<K, NXI, NROW, USK>;
     else
-      kern = near_sym_kernel<K, NXI, NROW>;
+      kern = near_sym_kernel<K, NXI, NROW, USK>;
     if (!carveout) {
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       cudaSharedmemCarveoutMaxShared),
@@ -718,6 +718,8 @@ template <class K>
 bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
                   const SymRange& r) {
   if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh, r), true;
+  // unskewed 3x3 (c1, c3, c5's cells): the fast tiles form each column's rx once per pair
+  if (a.nxi == 3 && a.nrow == 3 && a.unskewed && K::FAST) return launch_sym_shape<K, 3, 3, true>(a, st, fx, rsd, rsh, r), true;
   if (a.nxi == 3 && a.nrow == 3) return launch_sym_shape<K, 3, 3>(a, st, fx, rsd, rsh, r), true;
   if (a.nxi == 5 && a.nrow == 3) return launch_sym_shape<K, 5, 3>(a, st, fx, rsd, rsh, r), true;
   if (a.nxi == 7 && a.nrow == 3) return launch_sym_shape<K, 7, 3>(a, st, fx, rsd, rsh, r), true;

@@ -53,6 +53,7 @@ struct NearArgs {
   const int* out_row = nullptr;  // binned targets: output row of target l (nullptr: l)
   int lowp = 0;                  // near tiles: reduced-precision tier (eps >= 1e-11, pw_math.cuh)
   int cull = 1;                  // screened symmetric tiles: per-tile image mask (near_sym_impl.cuh)
+  int unskewed = 0;              // fused layout with shx[n][m] independent of n (xi == 0)
 };
 
 // ---------------------------------------------------------------- spatial binning (binning.cu)
