@@ -253,32 +253,46 @@ struct SymStokes {
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
-    double P = 1.0, txx = 0.0, txy = 0.0, px = 0.0, py = 0.0;
+    // Per image row n (common ry): S_n = sum_m 1/r^2, R_n = sum_m rx/r^2. Then
+    //   Tyy = sum_n ry_n^2 S_n, Txx = images - Tyy (rx^2/r^2 + ry^2/r^2 = 1 per image; no
+    //   exact zero on this path), Txy = sum_n ry_n R_n, pressurelet (sum_n R_n, sum_n ry_n S_n):
+    // two fp64 instructions per image besides the reciprocal, instead of three.
+    double P = 1.0, tyy = 0.0, txy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
+      double S = 0.0, R = 0.0;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
         const double rx = img_dx<NXI, NROW, USK>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
         const double inv = pwk::rcp_tier<LOWP>(r2);
-        const double xi = rx * inv;
-        txx = fma(xi, rx, txx);
-        txy = fma(xi, ry, txy);
-        if (PRESSURE) {
-          px += xi;
-          py = fma(ry, inv, py);
+        if (m == 0) {
+          S = inv;
+          R = rx * inv;
+        } else {
+          S += inv;
+          R = fma(rx, inv, R);
         }
+      }
+      if (n == 0) {
+        tyy = ry2 * S;
+        txy = ry * R;
+      } else {
+        tyy = fma(ry2, S, tyy);
+        txy = fma(ry, R, txy);
+      }
+      if (PRESSURE) {
+        px += R;
+        py = fma(ry, S, py);
       }
     }
     V[0] = pwk::log_fast(P, K, bad);
-    V[1] = txx;
+    V[1] = static_cast<double>(NXI * NROW) - tyy;
     V[2] = txy;
-    // rx^2/r^2 + ry^2/r^2 = 1 per image (no exact zero on this path): trace = image count,
-    // to ~2 ulp per image -- one DADD instead of an fma and a multiply per image
-    V[3] = static_cast<double>(NXI * NROW) - txx;
+    V[3] = tyy;
     if (PRESSURE) {
       V[4] = px;
       V[5] = py;

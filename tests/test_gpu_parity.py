@@ -522,7 +522,10 @@ def test_symmetric_tile_duplicates_and_image_coincidence(pw, gpu, pde, beta, str
     sym = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw)), key)
     one = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), **kw)), key)
     assert np.all(np.isfinite(sym))
-    assert rel_l2(sym, one) <= 1e-12
+    # both tiles run the reduced tier at eps = 1e-10 (reciprocal: MUFU seed + one linear
+    # step, ~1e-12 relative per image), each within 1e-12 of the full tier
+    # (test_symmetric_tile_tiers); their difference is bounded by the sum
+    assert rel_l2(sym, one) <= 2e-12
     bad = src.copy()
     bad[7] = [0.3, -0.5]
     bad[30000] = [0.3, 0.5]  # the (0, +1) image of point 7
