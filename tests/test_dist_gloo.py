@@ -144,7 +144,7 @@ def _system(pw):
     return pz, src, q
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, uneven=False):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -158,6 +158,9 @@ def _worker(rank, world, port, outdir):
 
     pz, src, q = _system(pw)
     be = NumpyBackend(pw, pz, src, q)
+    if uneven:  # a cost-balanced split (CudaBackend.near_split) need not be even: 80 / 20
+        items = be.near_items()[0]
+        be.near_split = lambda w: [0, (4 * items) // 5, items]
     plan = pdist.ShardPlan(len(src), len(src), world, rank)
     out, (lo, hi) = pdist.sharded_total_field(be, pdist.Comm(world), plan, symmetric=True)
     np.save(os.path.join(outdir, f"r{rank}.npy"), np.concatenate([[lo, hi], out.scalar.numpy()]))
@@ -247,3 +250,22 @@ def test_two_ranks_gloo_equal_one_rank(pw, port, tmp_path):
         be2.near_partial(lo, hi, part)
         halves += part
     assert np.array_equal(full.numpy(), halves.numpy())
+
+
+def test_two_ranks_gloo_uneven_item_split(pw, port, tmp_path):
+    """dist.sharded_total_field honours the backend's item bounds (pwb_near_sym_split's
+    cost-balanced ranges are uneven by count); the result equals the even split's."""
+    import torch.multiprocessing as mp
+
+    from paper_2111_01083_b200 import dist as pdist
+
+    world = 2
+    outs = {}
+    for uneven in (False, True):
+        d = tmp_path / ("u" if uneven else "e")
+        d.mkdir()
+        mp.start_processes(_worker, args=(world, _free_port(), str(d), uneven), nprocs=world, join=True,
+                           start_method="spawn")
+        outs[uneven] = np.concatenate([np.load(d / f"r{r}.npy")[2:] for r in range(world)])
+    a, b = outs[False], outs[True]
+    assert np.max(np.abs((a - a.mean()) - (b - b.mean()))) <= 1e-13 * np.max(np.abs(a))
