@@ -544,6 +544,15 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
         const int regime = a.cull ? pwk::regime_of(lo, hi, a.xcut2) : 0;
         auto sweep = [&](auto reg) {
           constexpr int R = decltype(reg)::value;
+          // regime sweeps: shifted targets once per image, (t - shift) - s (no coincidence is
+          // possible there); the per-pair dispatch keeps the reference's (t - s) - shift
+          // (apply.cpp:534), whose exact zeros decide CoincidentSourceTarget
+          double txs[TPT], tys[TPT];
+#pragma unroll
+          for (int k = 0; k < TPT; ++k) {
+            txs[k] = tx[k] - shx;
+            tys[k] = ty[k] - shy;
+          }
 #pragma unroll kMhSrcUnroll
           for (int i = 0; i < tn; ++i) {
             const double sx = s_x[i], sy = s_y[i];
@@ -551,8 +560,9 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
 #pragma unroll
             for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
 #pragma unroll
-            for (int k = 0; k < TPT; ++k) {  // (t - s) - shift, the reference's association (apply.cpp:534)
-              const double rx = (tx[k] - sx) - shx, ry = (ty[k] - sy) - shy;
+            for (int k = 0; k < TPT; ++k) {
+              const double rx = R == 0 ? (tx[k] - sx) - shx : txs[k] - sx;
+              const double ry = R == 0 ? (ty[k] - sy) - shy : tys[k] - sy;
               if constexpr (R == 0)
                 KER::image(acc[k], rx, ry, w, ident, a, flag);
               else

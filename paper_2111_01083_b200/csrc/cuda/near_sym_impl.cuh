@@ -533,6 +533,16 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         }
         auto sweep = [&](auto reg) {
           constexpr int R = decltype(reg)::value;
+          // regime sweeps (no coincidence possible, X_lo > 4): the shifted targets are formed
+          // once per image, (t - shift) - s, one subtraction per coordinate and pair; the
+          // per-pair dispatch keeps the reference's association (t - s) - shift
+          // (apply.cpp:534), whose exact zeros decide CoincidentSourceTarget
+          double txs[TPT], tys[TPT];
+#pragma unroll
+          for (int k = 0; k < TPT; ++k) {
+            txs[k] = tx[k] - shx;
+            tys[k] = ty[k] - shy;
+          }
 #pragma unroll kSymMhSrcUnroll
           for (int i = 0; i < TILE; ++i) {
             const int jj = (lane + i) & (TILE - 1);
@@ -546,8 +556,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
             for (int k = 0; k < TPT; ++k) {
               double V[K::NV];
-              // (t - s) - shift as upstream (apply.cpp:534)
-              const double rx = (tx[k] - sx) - shx, ry = (ty[k] - sy) - shy;
+              const double rx = R == 0 ? (tx[k] - sx) - shx : txs[k] - sx;
+              const double ry = R == 0 ? (ty[k] - sy) - shy : tys[k] - sy;
               if constexpr (R == 0) {
                 if (!K::image_value(V, rx, ry, ident, a, flag)) continue;
               } else {
