@@ -1,0 +1,14 @@
+# Second end-of-session set after the c2/c3/c5 tile changes (logs gpurun_out/fin2_*).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/fin2_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/fin2_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin2_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/fin2_smoke.log
+timeout 900 python bench.py > gpurun_out/fin2_bench_c4.log 2>&1
+for c in c1 c2 c3; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/fin2_bench_$c.log 2>&1; done
+echo "c5 slice: $(timeout 600 python tools/sort_experiment.py c5 --n 200000 --reps 2 | tail -1)" > gpurun_out/fin2_c5_slice.log
+timeout 1800 python tools/run_c5_full.py > gpurun_out/fin2_c5_full.json 2> gpurun_out/fin2_c5_full.err
+NCU="ncu --set full --clock-control none --import-source on"
+python tools/profile_step.py c2 --reps 1 > /dev/null 2>&1 && \
+  $NCU -k regex:near_tile -c 1 -f -o gpurun_out/fin2_c2_near_tile python tools/profile_step.py c2 --reps 1 > gpurun_out/fin2_ncu_c2.log 2>&1
+python tools/profile_step.py c3 --n 300000 --reps 1 > /dev/null 2>&1 && \
+  $NCU -k regex:near_sym -c 1 -f -o gpurun_out/fin2_c3_near_sym python tools/profile_step.py c3 --n 300000 --reps 1 > gpurun_out/fin2_ncu_c3.log 2>&1
+for f in gpurun_out/fin2_*.log gpurun_out/fin2_c5_full.json; do echo "== $f"; tail -n 2 "$f" | cut -c1-300; done
