@@ -432,12 +432,16 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const __grid_consta
   }
 }
 
+// out[i] = sum_b v[b * n + i]: one warp per value, lanes stride over the blocks, fixed-order
+// xor-shuffle tree (deterministic); a serial thread per value took ~20 us at 296 blocks
 __global__ void sum_blocks_kernel(const double* v, int blocks, int n, double* out) {
-  const int i = threadIdx.x;
+  const int i = static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n) return;
   double s = 0.0;
-  for (int b = 0; b < blocks; ++b) s += v[b * n + i];
-  out[i] = s;
+  for (int b = lane; b < blocks; b += 32) s += v[b * n + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[i] = s;
 }
 
 }  // namespace
@@ -450,6 +454,92 @@ void launch_s2pw(WeightSet ws, const S2pwArgs& a, cudaStream_t st) {
     case WeightSet::Force: return s2pw_dispatch<WeightSet::Force>(a, st);
     case WeightSet::ForceW: return s2pw_dispatch<WeightSet::ForceW>(a, st);
     case WeightSet::DoubleLayer: return s2pw_dispatch<WeightSet::DoubleLayer>(a, st);
+  }
+}
+
+// Small target counts (c1: 1000 targets = 8 blocks of the kernel above on 148 SMs): one
+// warp per target, lanes stride over the modes, fixed-order xor-shuffle reduction
+// (deterministic). Same per-(target, mode) arithmetic as pw2t_kernel.
+template <int KO, bool HASB, bool GRAD>
+__global__ void __launch_bounds__(kPw2tThreads) pw2t_warp_kernel(const __grid_constant__ Pw2tArgs a) {
+  const size_t l = (static_cast<size_t>(blockIdx.x) * kPw2tThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (l >= a.nt) return;  // whole warps leave together
+  const double2 t = a.tgt[l];
+  double acc[KO * 2 + 4];
+#pragma unroll
+  for (int v = 0; v < KO * 2 + 4; ++v) acc[v] = 0.0;
+  for (int r = lane; r < a.modes.count; r += 32) {
+    const int ax = a.modes.axis[r];
+    const double wc = ax ? t.x : t.y;
+    const double pc = ax ? t.y : t.x;
+    const double ph = a.modes.phase[r], dt = a.modes.decay_t[r];
+    const double mag = exp(dt * (wc - a.modes.shift_t[r]));
+    double sn, cs;
+    sincos(ph * pc, &sn, &cs);
+    const double tre = mag * cs, tim = mag * sn;
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      double cre = a.A[static_cast<size_t>(r) * KO * 2 + 2 * k], cim = a.A[static_cast<size_t>(r) * KO * 2 + 2 * k + 1];
+      if (HASB) {
+        cre = fma(wc, a.B[static_cast<size_t>(r) * KO * 2 + 2 * k], cre);
+        cim = fma(wc, a.B[static_cast<size_t>(r) * KO * 2 + 2 * k + 1], cim);
+      }
+      acc[2 * k] += tre * cre - tim * cim;
+      acc[2 * k + 1] += tre * cim + tim * cre;
+    }
+    if (GRAD) {
+      const double cre = a.A[static_cast<size_t>(r) * KO * 2], cim = a.A[static_cast<size_t>(r) * KO * 2 + 1];
+      const double pre = tre * cre - tim * cim, pim = tre * cim + tim * cre;
+      const double ire = -ph * pim, iim = ph * pre;
+      const double dre = dt * pre, dim = dt * pim;
+      double* g = acc + KO * 2;  // gx_re, gx_im, gy_re, gy_im
+      if (ax) {
+        g[0] += dre;
+        g[1] += dim;
+        g[2] += ire;
+        g[3] += iim;
+      } else {
+        g[0] += ire;
+        g[1] += iim;
+        g[2] += dre;
+        g[3] += dim;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int v = 0; v < KO * 2 + 4; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+  if (lane != 0) return;
+  double gx_re = acc[KO * 2], gy_re = acc[KO * 2 + 2];
+  if (a.m0_lin) {
+#pragma unroll
+    for (int v = 0; v < KO * 2; ++v) acc[v] = fma(t.y, a.m0_lin[v], acc[v]);
+    if (GRAD) gy_re += a.m0_lin[0];
+  }
+  if (a.m0_const) {
+#pragma unroll
+    for (int v = 0; v < KO * 2; ++v) acc[v] += a.m0_const[v];
+  }
+  if (a.out_re) {
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      double* dst = a.out_re + l * KO + k;
+      *dst = a.accumulate ? *dst + acc[2 * k] : acc[2 * k];
+    }
+  }
+  if (a.out_cplx) {
+#pragma unroll
+    for (int v = 0; v < KO * 2; ++v) {
+      double* dst = a.out_cplx + l * KO * 2 + v;
+      *dst = a.accumulate ? *dst + acc[v] : acc[v];
+    }
+  }
+  if (GRAD && a.out_grad) {
+    double* g = a.out_grad + 2 * l;
+    g[0] = a.accumulate ? g[0] + gx_re : gx_re;
+    g[1] = a.accumulate ? g[1] + gy_re : gy_re;
   }
 }
 
@@ -470,6 +560,26 @@ void launch_pw2t(const Pw2tArgs& a, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>((a.nt + kPw2tThreads - 1) / kPw2tThreads);
   const bool hasb = a.B != nullptr;
   count_launches(1);
+  int dev = 0, sms = 148;
+  cuda_check(cudaGetDevice(&dev), "device");
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  if (grid < static_cast<unsigned>(sms) && a.modes.count >= 64) {  // fewer blocks than SMs: a warp per target
+    const unsigned wgrid = static_cast<unsigned>((a.nt * 32 + kPw2tThreads - 1) / kPw2tThreads);
+    if (a.ko == 1) {
+      if (a.gradient)
+        pw2t_warp_kernel<1, false, true><<<wgrid, kPw2tThreads, 0, st>>>(a);
+      else if (hasb)
+        pw2t_warp_kernel<1, true, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
+      else
+        pw2t_warp_kernel<1, false, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
+    } else {
+      if (hasb)
+        pw2t_warp_kernel<2, true, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
+      else
+        pw2t_warp_kernel<2, false, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
+    }
+    return;
+  }
   if (a.ko == 1) {
     if (a.gradient)
       pw2t_kernel<1, false, true><<<grid, kPw2tThreads, 0, st>>>(a);
@@ -491,7 +601,7 @@ void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_che
 }
 
 void launch_sum_blocks(const double* block_vals, int blocks, int n, double* out, cudaStream_t st) {
-  sum_blocks_kernel<<<1, 32, 0, st>>>(block_vals, blocks, n, out);
+  sum_blocks_kernel<<<1, 32 * n, 0, st>>>(block_vals, blocks, n, out);
   count_launches(1);
 }
 

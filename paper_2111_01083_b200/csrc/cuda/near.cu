@@ -640,7 +640,7 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   // Source splits: the grid should cover >= 8 waves of resident blocks, with the
   // split count chosen so the last wave is as full as possible (ncu r1, c2: 782
   // blocks on 592 slots left the second wave 32 % occupied, fp64 pipe 61 %).
-  // Each split keeps >= 64 sources.
+  // Each split keeps >= 16 sources (c1: 1000 x 1000 runs 4 target blocks x 63 splits).
   static int resident = 0;  // per instantiation: blocks per SM at this kernel's registers/smem
   if (resident == 0) {
     int r = 0;
@@ -651,7 +651,7 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   const size_t slots = static_cast<size_t>(sm_count) * resident;
   int splits = 1;
   if (partial_ws != nullptr && bx < 8 * slots) {
-    const size_t max_by_src = (a.ns + 63) / 64;
+    const size_t max_by_src = (a.ns + 15) / 16;
     const int hi = static_cast<int>(std::min<size_t>({static_cast<size_t>(kMaxSplits), max_by_src,
                                                       (8 * slots + bx - 1) / bx + 8}));
     const int lo = std::max(1, std::min(hi, static_cast<int>((8 * slots + bx - 1) / bx)));
