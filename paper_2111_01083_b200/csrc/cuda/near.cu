@@ -632,6 +632,25 @@ __global__ void near_reduce_kernel(const double* partial, int splits, size_t nt,
   *dst += s;
 }
 
+// The same with one warp per output (small target counts with many splits: c1 sums 63
+// partials per output); lanes stride over the splits, fixed-order xor-shuffle tree.
+__global__ void near_reduce_warp_kernel(const double* partial, int splits, size_t nt, int nout, double* out0,
+                                        int nout0, double* out1, int nout1, const int* out_row) {
+  const size_t idx = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (idx >= nt * nout) return;
+  double s = 0.0;
+  for (int sp = lane; sp < splits; sp += 32) s += partial[static_cast<size_t>(sp) * nt * nout + idx];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
+  const size_t l = idx / nout;
+  const int c = static_cast<int>(idx % nout);
+  const size_t row = out_row ? static_cast<size_t>(out_row[l]) : l;
+  double* dst = c < nout0 ? out0 + row * nout0 + c : out1 + row * nout1 + (c - nout0);
+  *dst += s;
+}
+
 template <class KER, int NXI, int NROW, int TPT>
 void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int sm_count) {
   NearArgs a = a0;
@@ -675,8 +694,13 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   count_launches(1);
   if (splits > 1) {
     const size_t n = a.nt * KER::NOUT;
-    near_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(partial_ws, splits, a.nt, KER::NOUT,
-                                                                               a.out0, a.nout0, a.out1, a.nout1, a.out_row);
+    if (n < 65536 && splits >= 8)
+      near_reduce_warp_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, st>>>(
+          partial_ws, splits, a.nt, KER::NOUT, a.out0, a.nout0, a.out1, a.nout1, a.out_row);
+    else
+      near_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(partial_ws, splits, a.nt, KER::NOUT,
+                                                                                 a.out0, a.nout0, a.out1, a.nout1,
+                                                                                 a.out_row);
     count_launches(1);
   }
 }
