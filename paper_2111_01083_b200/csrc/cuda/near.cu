@@ -25,9 +25,6 @@
 #include "pw_pair.cuh"
 #include "near_common.cuh"
 
-#ifndef PWB_MH_UNROLL_M
-#define PWB_MH_UNROLL_M 3  // image columns per unrolled step (screened kernels; c2: 1 -> 929 ms, 2 -> 807, 3 -> 792, 5 -> 890)
-#endif
 #ifndef PWB_MH_SRC_UNROLL
 #define PWB_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c2: 2 -> 579 ms, 4 -> 566)
 #endif
@@ -36,7 +33,6 @@
 #endif
 namespace pwb {
 namespace {
-constexpr int kMhUnrollM = PWB_MH_UNROLL_M;
 constexpr int kMhSrcUnroll = PWB_MH_SRC_UNROLL;
 }
 }  // namespace pwb
@@ -104,28 +100,6 @@ template <bool LOWP>
 struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
   static constexpr int NW = 1, NACC = 1, NOUT = 1;
   static constexpr bool EXP_TAB = LOWP;  // k01_tile<true, .> reads the shared exp table
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
-                                              const NearArgs& a, int& flag) {
-#pragma unroll 1  // rows rolled: long Bessel body per image (see near_sym_impl.cuh)
-    for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
-      const double ry2 = ry * ry;
-#pragma unroll kMhUnrollM
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double r2 = fma(rx, rx, ry2);
-        if (r2 == 0.0) {
-          if (rx == 0.0 && ry == 0.0) {
-            if (n * NXI + m != a.id_img) flag = 1;
-            continue;
-          }
-        }
-        const double X = a.beta2 * r2;
-        if (X < a.xcut2) acc[0] = fma(w[0], pwk::k01_tile<LOWP, false>(X).k0, acc[0]);
-      }
-    }
-  }
   // one image of one pair (image-outer loop of near_tile_kernel): same semantics as pair()
   static constexpr bool IMAGE_OUTER = true;
   __device__ __forceinline__ static void image(double* acc, double rx, double ry, const double* w, bool ident,
@@ -156,34 +130,6 @@ template <bool LOWP>
 struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
   static constexpr int NW = 1, NACC = 3, NOUT = 3;
   static constexpr bool EXP_TAB = LOWP;
-  template <int NXI, int NROW>
-  __device__ __forceinline__ static void pair(double* acc, double dx, double dy, const double* w,
-                                              const NearArgs& a, int& flag) {
-#pragma unroll 1  // rows rolled: long Bessel body per image (see near_sym_impl.cuh)
-    for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
-      const double ry2 = ry * ry;
-#pragma unroll kMhUnrollM
-      for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double r2 = fma(rx, rx, ry2);
-        if (r2 == 0.0) {
-          if (rx == 0.0 && ry == 0.0) {
-            if (n * NXI + m != a.id_img) flag = 1;
-            continue;
-          }
-        }
-        const double X = a.beta2 * r2;
-        if (X < a.xcut2) {
-          const pwk::K01 k = pwk::k01_tile<LOWP, true>(X);
-          acc[0] = fma(w[0], k.k0, acc[0]);
-          const double g = w[0] * k.k1_over_x;
-          acc[1] = fma(g, rx, acc[1]);
-          acc[2] = fma(g, ry, acc[2]);
-        }
-      }
-    }
-  }
   static constexpr bool IMAGE_OUTER = true;
   __device__ __forceinline__ static void image(double* acc, double rx, double ry, const double* w, bool ident,
                                                const NearArgs& a, int& flag) {
@@ -577,21 +523,21 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
         else
           sweep(std::integral_constant<int, 0>{});
       }
-      continue;
-    }
+    } else {
 #pragma unroll 2
-    for (int i = 0; i < tn; ++i) {
-      const double sx = s_x[i], sy = s_y[i];
-      double w[KER::NW];
+      for (int i = 0; i < tn; ++i) {
+        const double sx = s_x[i], sy = s_y[i];
+        double w[KER::NW];
 #pragma unroll
-      for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
+        for (int c = 0; c < KER::NW; ++c) w[c] = s_w[c][i];
 #pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        // (t - s) - shift, the reference's association (apply.cpp:534)
-        if constexpr (HasConsts<KER>::value)
-          KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag, C);
-        else
-          KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag);
+        for (int k = 0; k < TPT; ++k) {
+          // (t - s) - shift, the reference's association (apply.cpp:534)
+          if constexpr (HasConsts<KER>::value)
+            KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag, C);
+          else
+            KER::template pair<NXI, NROW>(acc[k], tx[k] - sx, ty[k] - sy, w, a, flag);
+        }
       }
     }
   }
