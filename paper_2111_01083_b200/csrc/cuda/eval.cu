@@ -140,7 +140,7 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
     }
     case 8: {  // the reduced tier's table-driven log (pw_math.cuh log_tab), table read unreplicated
       unsigned bad = 0;
-      out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts(pwk::pw_log_tab_dev_ptr(), 0), bad);
+      out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts<1>(pwk::pw_log_tab_dev_ptr(), 0), bad);
       break;
     }
     default:

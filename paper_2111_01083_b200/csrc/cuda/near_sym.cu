@@ -42,10 +42,11 @@ size_t near_sym_tiles(size_t n) { return (n + 255) / 256; }
 namespace {
 template <class K>
 long item_count(size_t n) {
-  const size_t tile = static_cast<size_t>(sym::kT) * K::TPT;
-  const long nb = static_cast<long>((n + tile - 1) / tile);
+  const size_t tile = static_cast<size_t>(sym::kT) * K::TPT, ct = static_cast<size_t>(sym::kT) * K::CPT;
+  const long nb = static_cast<long>((n + tile - 1) / tile), ncb = static_cast<long>((n + ct - 1) / ct);
+  const long r = static_cast<long>(tile / ct);
   long items = 0;
-  for (long I = 0; I < nb; ++I) items += (nb - I + K::CHUNK - 1) / K::CHUNK;
+  for (long I = 0; I < nb; ++I) items += (ncb - I * r + K::CHUNK - 1) / K::CHUNK;
   return items;
 }
 // ---- cost-balanced item ranges for the multi-GPU split of the screened tiles ----------
@@ -148,6 +149,7 @@ __global__ void split_kernel(const float* __restrict__ prefix, long items, int w
 void near_sym_shape(NearKind kind, int* tile, int* chunk) {
   auto set = [&](auto k) {
     using K = decltype(k);
+    static_assert(K::CPT == K::TPT || !K::CULL, "the cost split assumes square tiles");
     *tile = sym::kT * K::TPT;
     *chunk = K::CHUNK;
   };

@@ -62,6 +62,12 @@ namespace sym {
 #ifndef PWB_SYM_LOG_TABLE
 #define PWB_SYM_LOG_TABLE 1  // reduced tier: table-driven ln (pw_math.cuh log_tab) instead of log_pos_k<true>
 #endif
+#ifndef PWB_SYM_LAPLACE_CPT
+#define PWB_SYM_LAPLACE_CPT 2  // column points per thread of the Laplace tile (column tile 128 * CPT)
+#endif
+#ifndef PWB_SYM_LAPLACE_REPL
+#define PWB_SYM_LAPLACE_REPL 8  // log-table replicas of the Laplace tile (8: conflict-free LDS.128)
+#endif
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
 #endif
@@ -94,9 +100,14 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
 
 template <bool LOWP_>
 struct SymLaplace {
-  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT, CHUNK = 8,
+  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT,
+                       CHUNK = 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
+  // 256-point column tiles under the 512-point row tile: the staged sources and per-warp
+  // column partials take 14 KB, so the conflict-free 8-replica log table (16 KB) fits
+  // 6 blocks per SM
+  static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = PWB_SYM_LAPLACE_REPL;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -149,6 +160,7 @@ struct SymModHelm {
   static constexpr bool FAST = false, LOWP = LOWP_;
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
+  static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
   // mask: bit n * NXI + m set for the images that may hold a pair with beta r < 64 in this
@@ -248,7 +260,7 @@ struct SymModHelm {
 template <bool PRESSURE, bool LOWP_>
 struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
-                       CHUNK = 16, MINB = 0, UNROLL = 2;
+                       CHUNK = 16, MINB = 0, UNROLL = 2, CPT = TPT, LOG_REPL = pwk::kLogTabReplicas;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -351,7 +363,8 @@ struct SymStokes {
 // ---------------------------------------------------------------- the kernel
 struct SymArgs {
   NearArgs a;
-  int nb;                  // number of TILE-point tiles
+  int nb;                  // number of row tiles (kT * TPT points)
+  int ncb;                 // number of column tiles (kT * CPT points)
   int chunk;               // column tiles per work item
   const int* row_start;    // [nb + 1] first work item of each row tile
   unsigned long long* fx;  // fixed-point accumulators [n][nout][3]
@@ -397,10 +410,13 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
 template <class K, int NXI, int NROW, bool USK>
 __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   constexpr int TPT = K::TPT;
-  constexpr int TILE = kT * TPT;
+  constexpr int TILE = kT * TPT;      // row tile: the block's targets
+  constexpr int CT = kT * K::CPT;     // column tile: the sources staged per step
+  constexpr int R = TILE / CT;        // column tiles per row tile
+  static_assert(TILE % CT == 0 && (CT & (CT - 1)) == 0, "column tile must divide the row tile");
   const NearArgs& a = S.a;
-  __shared__ double s_x[TILE], s_y[TILE], s_w[K::NW][TILE];
-  __shared__ double s_col[kWarps][K::NACC][TILE];
+  __shared__ double s_x[CT], s_y[CT], s_w[K::NW][CT];
+  __shared__ double s_col[kWarps][K::NACC][CT];
 
   // work item -> (row tile I, first column tile)
   const int item = S.item0 + static_cast<int>(blockIdx.x);
@@ -413,8 +429,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       hi = mid;
   }
   const int I = lo;
-  const int J0 = I + (item - S.row_start[I]) * S.chunk;
-  const int J1 = min(S.nb, J0 + S.chunk);
+  const int J0 = I * R + (item - S.row_start[I]) * S.chunk;
+  const int J1 = min(S.ncb, J0 + S.chunk);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t n = a.nt;
@@ -433,15 +449,16 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   }
   int flag = 0;
   // log constants in registers; the reduced tier's log table in shared memory
-  constexpr size_t kTileSmem = sizeof(double) * (static_cast<size_t>(TILE) * (2 + K::NW) + kWarps * K::NACC * TILE);
-  constexpr size_t kTabSmem = sizeof(double2) * pwk::kLogTabEntries * pwk::kLogTabReplicas;
+  constexpr size_t kTileSmem = sizeof(double) * (static_cast<size_t>(CT) * (2 + K::NW) + kWarps * K::NACC * CT);
+  constexpr int kRepl = K::LOG_REPL;
+  constexpr size_t kTabSmem = sizeof(double2) * pwk::kLogTabEntries * kRepl;
   constexpr bool kTab = K::FAST && K::LOWP && PWB_SYM_LOG_TABLE && kTileSmem + kTabSmem <= 48 * 1024;
-  __shared__ double2 s_lt[kTab ? pwk::kLogTabEntries * pwk::kLogTabReplicas : 1];
-  using LKT = std::conditional_t<kTab, pwk::LogT, pwk::LogK<K::LOWP>>;
+  __shared__ double2 s_lt[kTab ? pwk::kLogTabEntries * kRepl : 1];
+  using LKT = std::conditional_t<kTab, pwk::LogT<kRepl>, pwk::LogK<K::LOWP>>;
   LKT LK;
   if constexpr (kTab) {
-    pwk::log_tab_fill(s_lt, tid, kT);  // visible after the first __syncthreads of the tile loop
-    LK = pwk::log_tab_consts(s_lt, lane);
+    pwk::log_tab_fill<kRepl>(s_lt, tid, kT);  // visible after the first __syncthreads of the tile loop
+    LK = pwk::log_tab_consts<kRepl>(s_lt, lane);
   } else if constexpr (K::FAST) {
     LK = pwk::log_consts<K::LOWP>();
   }
@@ -462,10 +479,10 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   }
 
   for (int J = J0; J < J1; ++J) {
-    const size_t jbase = static_cast<size_t>(J) * TILE;
+    const size_t jbase = static_cast<size_t>(J) * CT;
     __syncthreads();
     double cb[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-    for (int i = tid; i < TILE; i += kT) {
+    for (int i = tid; i < CT; i += kT) {
       const size_t j = jbase + i;
       const bool lv = j < n;
       const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);
@@ -499,8 +516,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       mask = image_mask<NXI, NROW>(rb, cbx, a);
       if (mask == 0u) continue;  // block-uniform: no pair of this tile pair is in range
     }
-    if (J == I) {  // diagonal tile: one-sided and careful (self pairs live here)
-      for (int i = 0; i < TILE; ++i) {
+    if (J < (I + 1) * R) {  // inside the row tile: one-sided and careful (self pairs live here)
+      for (int i = 0; i < CT; ++i) {
         const double sx = s_x[i], sy = s_y[i];
         double w[K::NW];
 #pragma unroll
@@ -544,8 +561,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
             tys[k] = ty[k] - shy;
           }
 #pragma unroll kSymMhSrcUnroll
-          for (int i = 0; i < TILE; ++i) {
-            const int jj = (lane + i) & (TILE - 1);
+          for (int i = 0; i < CT; ++i) {
+            const int jj = (lane + i) & (CT - 1);
             const double sx = s_x[jj], sy = s_y[jj];
             double w[K::NW];
 #pragma unroll
@@ -587,8 +604,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         for (int c = 0; c < K::NACC; ++c) keep[k][c] = racc[k][c];
       std::conditional_t<kTab, unsigned, int> bad = 0;  // see pwk::log_bad
 #pragma unroll K::UNROLL
-      for (int i = 0; i < TILE; ++i) {
-        const int jj = (lane + i) & (TILE - 1);
+      for (int i = 0; i < CT; ++i) {
+        const int jj = (lane + i) & (CT - 1);
         const double sx = s_x[jj], sy = s_y[jj];
         double w[K::NW];
 #pragma unroll
@@ -612,7 +629,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         for (int k = 0; k < TPT; ++k)
 #pragma unroll
           for (int c = 0; c < K::NACC; ++c) racc[k][c] = keep[k][c];
-        for (int i = tid; i < TILE; i += kT)
+        for (int i = tid; i < CT; i += kT)
 #pragma unroll
           for (int c = 0; c < K::NACC; ++c)
 #pragma unroll
@@ -623,8 +640,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     }
     if (careful) {
 #pragma unroll 1
-      for (int i = 0; i < TILE; ++i) {
-        const int jj = (lane + i) & (TILE - 1);
+      for (int i = 0; i < CT; ++i) {
+        const int jj = (lane + i) & (CT - 1);
         const double sx = s_x[jj], sy = s_y[jj];
         double w[K::NW];
 #pragma unroll
@@ -645,7 +662,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     }
     __syncthreads();
     // column totals of this tile -> fixed point
-    for (int i = tid; i < TILE; i += kT) {
+    for (int i = tid; i < CT; i += kT) {
       const size_t j = jbase + i;
       if (j >= n) continue;
       double acc[K::NACC];
@@ -692,13 +709,14 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
 template <class K, int NXI, int NROW, bool USK = false>
 void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
                       int* row_start_host, const SymRange& range) {
-  constexpr int TILE = kT * K::TPT;
+  constexpr int TILE = kT * K::TPT, CT = kT * K::CPT, R = TILE / CT;
   const int chunk = K::CHUNK;
   const int nb = static_cast<int>((a.nt + TILE - 1) / TILE);
+  const int ncb = static_cast<int>((a.nt + CT - 1) / CT);
   int items = 0;
   for (int I = 0; I < nb; ++I) {
     row_start_host[I] = items;
-    items += (nb - I + chunk - 1) / chunk;
+    items += (ncb - I * R + chunk - 1) / chunk;
   }
   row_start_host[nb] = items;
   if (range.total_items) *range.total_items = items;
@@ -712,6 +730,7 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
   SymArgs S;
   S.a = a;
   S.nb = nb;
+  S.ncb = ncb;
   S.chunk = chunk;
   S.row_start = row_start_dev;
   S.fx = fx;
