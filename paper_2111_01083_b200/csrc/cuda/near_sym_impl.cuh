@@ -63,13 +63,13 @@ namespace sym {
 #define PWB_SYM_LOG_TABLE 1  // reduced tier: table-driven ln (pw_math.cuh log_tab) instead of log_pos_k<true>
 #endif
 #ifndef PWB_SYM_LAPLACE_CPT
-#define PWB_SYM_LAPLACE_CPT 2  // column points per thread of the Laplace tile (column tile 128 * CPT)
+#define PWB_SYM_LAPLACE_CPT 1  // column points per thread of the Laplace tile (column tile 128 * CPT; c4: 4 -> 669 ms, 2 -> 667, 1 at 7 blocks -> 653)
 #endif
 #ifndef PWB_SYM_LAPLACE_REPL
 #define PWB_SYM_LAPLACE_REPL 8  // log-table replicas of the Laplace tile (8: conflict-free LDS.128)
 #endif
 #ifndef PWB_SYM_LAPLACE_MINB
-#define PWB_SYM_LAPLACE_MINB 6  // 6 x 4 warps/SM (80 regs, no spills since the log rewrite): c4 918.9 -> 905.7 ms vs 5
+#define PWB_SYM_LAPLACE_MINB 7  // 7 x 4 warps/SM at 72 registers (128-point column tiles leave room in shared memory): c4 667 -> 653 ms vs 6
 #endif
 constexpr int kT = 128;  // threads per block
 constexpr int kSymMhUnrollM = PWB_SYM_MH_UNROLL_M;
@@ -104,9 +104,9 @@ struct SymLaplace {
                        CHUNK = 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
-  // 256-point column tiles under the 512-point row tile: the staged sources and per-warp
-  // column partials take 14 KB, so the conflict-free 8-replica log table (16 KB) fits
-  // 6 blocks per SM
+  // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
+  // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
+  // blocks per SM fit
   static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = PWB_SYM_LAPLACE_REPL;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,

@@ -199,10 +199,10 @@ def test_item_counts_match_the_device_decomposition(pw):
     pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-10)
     for n, want in ((1, 1), (512, 1), (513, 2), (1000000, None)):
         items, nout = pw.near_sym_items(pz, n)
-        # Laplace: 512-point row tiles (4 targets x 128 threads), 256-point column tiles,
-        # 16 column tiles per item; row tile I starts at column tile 2 I
-        nb, ncb = (n + 511) // 512, (n + 255) // 256
-        assert items == sum((ncb - 2 * i + 15) // 16 for i in range(nb))
+        # Laplace: 512-point row tiles (4 targets x 128 threads), 128-point column tiles,
+        # 32 column tiles (4096 sources) per item; row tile I starts at column tile 4 I
+        nb, ncb = (n + 511) // 512, (n + 127) // 128
+        assert items == sum((ncb - 4 * i + 31) // 32 for i in range(nb))
         assert nout == 1
         if want is not None:
             assert items == want
