@@ -36,8 +36,8 @@ void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int 
   count_launches(1);
 }
 
-// upper bound on the number of tiles (the smallest tile is 256 points)
-size_t near_sym_tiles(size_t n) { return (n + 255) / 256; }
+// upper bound on the number of row tiles (the smallest row tile is 128 points)
+size_t near_sym_tiles(size_t n) { return (n + 127) / 128; }
 
 namespace {
 template <class K>

@@ -68,6 +68,15 @@ namespace sym {
 #ifndef PWB_SYM_LAPLACE_REPL
 #define PWB_SYM_LAPLACE_REPL 8  // log-table replicas of the Laplace tile (8: conflict-free LDS.128)
 #endif
+#ifndef PWB_SYM_STOKES_TPT
+#define PWB_SYM_STOKES_TPT 2  // targets per thread of the Stokeslet tile
+#endif
+#ifndef PWB_SYM_STOKES_CPT
+#define PWB_SYM_STOKES_CPT 2  // column points per thread of the Stokeslet tile
+#endif
+#ifndef PWB_SYM_STOKES_MINB
+#define PWB_SYM_STOKES_MINB 0  // 0: ptxas's own register allocation (166 registers, 3 blocks/SM)
+#endif
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 7  // 7 x 4 warps/SM at 72 registers (128-point column tiles leave room in shared memory): c4 667 -> 653 ms vs 6
 #endif
@@ -259,8 +268,11 @@ struct SymModHelm {
 // P = sum r / r^2 (pressurelet, odd).
 template <bool PRESSURE, bool LOWP_>
 struct SymStokes {
-  static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2, TPT = 2,
-                       CHUNK = 16, MINB = 0, UNROLL = 2, CPT = TPT, LOG_REPL = pwk::kLogTabReplicas;
+  static constexpr int NW = 2, NV = PRESSURE ? 6 : 4, NACC = PRESSURE ? 5 : 4, NOUT = PRESSURE ? 3 : 2,
+                       TPT = PWB_SYM_STOKES_TPT, CPT = PWB_SYM_STOKES_CPT < PWB_SYM_STOKES_TPT ? PWB_SYM_STOKES_CPT
+                                                                                                : PWB_SYM_STOKES_TPT,
+                       CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
+                       LOG_REPL = pwk::kLogTabReplicas;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
