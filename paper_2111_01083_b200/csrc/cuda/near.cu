@@ -28,6 +28,12 @@
 #ifndef PWB_MH_SRC_UNROLL
 #define PWB_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c2: 2 -> 579 ms, 4 -> 566)
 #endif
+#ifndef PWB_MH_GEN_UNROLL
+#define PWB_MH_GEN_UNROLL 1  // sources per unrolled step of the per-pair-dispatch sweep
+#endif
+#ifndef PWB_MH_NEAR_SWEEP
+#define PWB_MH_NEAR_SWEEP 0  // 1: a tile pair wholly in 2 <= x < 6 gets its own sweep (c2: 520 ms vs 512 without: smaller code wins)
+#endif
 #ifndef PWB_MH_TPT
 #define PWB_MH_TPT 1  // targets per thread of the screened one-sided tiles
 #endif
@@ -499,7 +505,8 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
             txs[k] = tx[k] - shx;
             tys[k] = ty[k] - shy;
           }
-#pragma unroll kMhSrcUnroll
+          constexpr int kU = R == 0 ? PWB_MH_GEN_UNROLL : kMhSrcUnroll;  // the per-pair dispatch is branchy: less unrolled
+#pragma unroll kU
           for (int i = 0; i < tn; ++i) {
             const double sx = s_x[i], sy = s_y[i];
             double w[KER::NW];
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(kThreads) near_tile_kernel(const __grid_consta
         };
         if (regime == 2)
           sweep(std::integral_constant<int, 2>{});
-        else if (regime == 1)
+        else if (regime == 1 && PWB_MH_NEAR_SWEEP)
           sweep(std::integral_constant<int, 1>{});
         else
           sweep(std::integral_constant<int, 0>{});

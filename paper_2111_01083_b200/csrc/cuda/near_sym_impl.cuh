@@ -53,6 +53,12 @@ namespace sym {
 #ifndef PWB_SYM_MH_SRC_UNROLL
 #define PWB_SYM_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c5 slice: 2 -> 159 ms, 4 -> 154)
 #endif
+#ifndef PWB_SYM_MH_GEN_UNROLL
+#define PWB_SYM_MH_GEN_UNROLL 1  // sources per unrolled step of the per-pair-dispatch sweep (c5 slice: 4 -> 153.6 ms, 1 -> 143.7)
+#endif
+#ifndef PWB_SYM_MH_NEAR_SWEEP
+#define PWB_SYM_MH_NEAR_SWEEP 1  // 1: a tile pair wholly in 2 <= x < 6 gets its own branch-free sweep (c5: 143.7 vs 153.0 without)
+#endif
 #ifndef PWB_SYM_MH_TPT
 #define PWB_SYM_MH_TPT 2  // targets per thread of the screened symmetric tile
 #endif
@@ -572,7 +578,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
             txs[k] = tx[k] - shx;
             tys[k] = ty[k] - shy;
           }
-#pragma unroll kSymMhSrcUnroll
+          constexpr int kU = R == 0 ? PWB_SYM_MH_GEN_UNROLL : kSymMhSrcUnroll;  // the per-pair dispatch is branchy: less unrolled
+#pragma unroll kU
           for (int i = 0; i < CT; ++i) {
             const int jj = (lane + i) & (CT - 1);
             const double sx = s_x[jj], sy = s_y[jj];
@@ -601,7 +608,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         };
         if (regime == 2)
           sweep(std::integral_constant<int, 2>{});
-        else if (regime == 1)
+        else if (regime == 1 && PWB_SYM_MH_NEAR_SWEEP)
           sweep(std::integral_constant<int, 1>{});
         else
           sweep(std::integral_constant<int, 0>{});
