@@ -36,7 +36,7 @@ F_FAR = {"c1": 70, "c2": 70, "c3": 86, "c4": 70, "c5": 70}
 # (tools/sass_loop_stats.py), per log tier: the reduced tier runs when eps >= 1e-11 unless
 # PWB_FULL_PRECISION is set (pw_math.cuh log_pos_k)
 FP64_INSTR_PER_GROUP = {("c4", "full"): 29.25, ("c4", "reduced"): 18.25,
-                        ("c3", "full"): 106.0, ("c3", "reduced"): 86.0}
+                        ("c3", "full"): 103.0, ("c3", "reduced"): 83.0}
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_traffic.json")
 
 
