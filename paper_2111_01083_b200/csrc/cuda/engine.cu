@@ -845,6 +845,9 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
   // orders below eps for eps >= 1e-11 (the reference's eps bounds the far truncation);
   // the full tier is ~1 ulp. PWB_FULL_PRECISION forces the full tier (tests).
   a.lowp = (pz_.eps >= 1e-11 && std::getenv("PWB_FULL_PRECISION") == nullptr) ? 1 : 0;
+  // coarse Bessel tier of the symmetric screened tile: <= ~1e-11 relative per K0 / K1, three
+  // orders below eps >= 1e-9 (c5: eps = 1e-8); PWB_NO_COARSE keeps the reduced tier
+  if (a.lowp && pz_.eps >= 1e-9 && std::getenv("PWB_NO_COARSE") == nullptr) a.lowp = 2;
   a.cull = std::getenv("PWB_NO_CULL") == nullptr ? 1 : 0;  // A/B and the exactness test only
   if (kind == Kind::Multipole) {
     nk = NearKind::Multipole;

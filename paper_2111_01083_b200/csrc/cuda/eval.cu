@@ -138,6 +138,13 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       out[4 * i + 3] = r.k1_over_x * x;
       break;
     }
+    case 9: {  // the coarse tier of the symmetric screened tile (x < 64)
+      const double x = in[i];
+      const pwk::K01 c = pwk::k01_tile<true, true, true>(x * x);
+      out[2 * i] = c.k0;
+      out[2 * i + 1] = c.k1_over_x * x;
+      break;
+    }
     case 8: {  // the reduced tier's table-driven log (pw_math.cuh log_tab), table read unreplicated
       unsigned bad = 0;
       out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts<1>(pwk::pw_log_tab_dev_ptr(), 0), bad);
@@ -200,7 +207,7 @@ double fp64_peak_probe() {
 
 int eval_in_width(int which) { return (which == 0 || which >= 6) ? 1 : which == 5 ? 4 : 2; }
 int eval_out_width(int which) {
-  return (which <= 1 || which == 8) ? 1 : (which == 3 || which == 4) ? 2 : which == 6 ? 6 : 4;
+  return (which <= 1 || which == 8) ? 1 : (which == 3 || which == 4 || which == 9) ? 2 : which == 6 ? 6 : 4;
 }
 
 void run_eval(int which, int pde, double beta, int l, size_t n, const double* in_host, double* out_host) {

@@ -168,8 +168,8 @@ struct SymLaplace {
   }
 };
 
-template <bool GRAD, bool LOWP_>
-struct SymModHelm {
+template <bool GRAD, bool LOWP_, bool COARSE = false>
+struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr int NW = 1, NV = GRAD ? 3 : 1, NACC = NV, NOUT = NV, TPT = PWB_SYM_MH_TPT, CHUNK = 16, MINB = 0,
                        UNROLL = 1;
   static constexpr bool FAST = false, LOWP = LOWP_;
@@ -205,7 +205,7 @@ struct SymModHelm {
         }
         const double X = a.beta2 * r2;
         if (X < a.xcut2) {
-          const pwk::K01 k = pwk::k01_tile<LOWP, GRAD>(X);
+          const pwk::K01 k = pwk::k01_tile<LOWP, GRAD, COARSE>(X);
           V[0] += k.k0;
           if (GRAD) {
             V[1] = fma(k.k1_over_x, rx, V[1]);
@@ -229,7 +229,7 @@ struct SymModHelm {
     }
     const double X = a.beta2 * r2;
     if (!pwk::lt_hi(X, a.xcut2)) return false;  // xcut2 has a zero low word (engine.cu)
-    const pwk::K01 k = pwk::k01_tile<LOWP, GRAD>(X);
+    const pwk::K01 k = pwk::k01_tile<LOWP, GRAD, COARSE>(X);
     V[0] = k.k0;
     if (GRAD) {
       V[1] = k.k1_over_x * rx;
@@ -242,7 +242,7 @@ struct SymModHelm {
   template <bool FAR>
   __device__ __forceinline__ static void image_fast(double* V, double rx, double ry, const NearArgs& a) {
     const double X = a.beta2 * fma(rx, rx, ry * ry);
-    const pwk::K01 k = pwk::k01_asym<LOWP, GRAD, FAR>(X);
+    const pwk::K01 k = pwk::k01_asym<LOWP, GRAD, FAR, COARSE>(X);
     V[0] = k.k0;
     if (GRAD) {
       V[1] = k.k1_over_x * rx;

@@ -498,6 +498,17 @@ def test_hot_tile_bessel_tiers(pw, gpu, ref):
         assert np.all(low <= 2e-13 + 3e-16 * xs), (l, xs[np.argmax(low)], low.max())
 
 
+def test_hot_tile_bessel_coarse_tier(pw, gpu, ref):
+    """The symmetric screened tile's coarse tier (eps >= 1e-9, c5): 9 + 8 term asymptotic
+    polynomials and a degree-3 e^r, <= ~1e-11 relative to the reference's Bessel functions."""
+    xs = np.concatenate([np.geomspace(2.0, 63.99, 500), [2.0000001, 5.999999, 6.0, 6.0000001]])
+    out = pw.eval_kernel(9, 0, 0.0, 0, xs)
+    for l in (0, 1):
+        want = np.array([ref.bessel_kn(l, x) for x in xs])
+        rel = np.abs(out[:, l] - want) / want
+        assert np.all(rel <= 3e-11 + 3e-16 * xs), (l, xs[np.argmax(rel)], rel.max())
+
+
 @pytest.mark.parametrize("pde,beta,strength", [("Poisson", 0.0, "charge"), ("ModHelmholtz", 2.0, "charge"),
                                                ("Stokes", 0.0, "force")])
 def test_symmetric_tile_duplicates_and_image_coincidence(pw, gpu, pde, beta, strength):
