@@ -47,7 +47,10 @@ namespace pwb {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kTile = 256;
+#ifndef PWB_NEAR_TILE
+#define PWB_NEAR_TILE 256  // sources staged per step of the one-sided tile
+#endif
+constexpr int kTile = PWB_NEAR_TILE;
 
 // ---------------------------------------------------------------- pair functors
 // Each functor: NW strength doubles per source, NACC accumulators per target,
