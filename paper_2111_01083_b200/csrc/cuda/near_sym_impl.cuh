@@ -10,10 +10,16 @@
 // identity-image self pairs are skipped, any other coincidence sets the flag.
 //
 // Work items: row tile I (TILE = 128 * TPT points, TPT per thread) x a chunk of
-// column tiles J >= I (the diagonal tile runs one-sided). Column partials use a
-// rotating schedule (lane l reads column (l + i) mod TILE, one private column
-// copy per warp) so no two lanes of a warp touch the same column and no atomics
-// are needed inside the block.
+// column tiles (CT = 128 * CPT points, CT dividing TILE) starting at the row tile's
+// own first column tile; the column tiles inside the row tile run one-sided (each
+// ordered pair once, self pairs included), the ones beyond it symmetric. Column
+// partials use a rotating schedule (lane l reads column (l + i) mod CT, one private
+// column copy per warp) so no two lanes of a warp touch the same column and no
+// atomics are needed inside the block.
+//
+// Screened kernels (modified Helmholtz): off-diagonal tile pairs run image-outer
+// sweeps with a per-tile-pair image mask and regime (bounding boxes of both tiles),
+// see the CULL functor and DESIGN.md §3.1 items 8-10.
 //
 // Fast path: for kernels whose per-pair work is a product of image distances
 // (Laplace log, Stokeslet) the off-diagonal tiles run branch-free; a pair whose
