@@ -353,10 +353,11 @@ def test_symmetric_targets_equal_sources(pw, gpu, ref, name, n):
     assert rel_l2(sym[idx], want, gauge) <= 10 * c.eps
 
 
+@pytest.mark.parametrize("eps", [1e-8, 1e-12])
 @pytest.mark.parametrize("sym", [True, False])
 @pytest.mark.parametrize("grad", [False, True])
 @pytest.mark.parametrize("cellt,beta", [((100.0, 0.0, 1.0, 2), 1.0), ((1.0, 0.3, 0.8, 2), 10.0)])
-def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad, sym, cellt, beta):
+def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad, sym, cellt, beta, eps):
     """The screened tiles drop, per tile pair, the images whose bounding-box gap puts every
     pair beyond the K0 cut-off, and run a tile pair whose box range lies in one asymptotic
     regime without the per-pair dispatch (near_sym_impl.cuh, near.cu; pw_math.cuh
@@ -372,7 +373,8 @@ def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad, sym, cellt,
     u = rng.uniform(-0.5, 0.5, (n, 2))
     src = np.ascontiguousarray(np.column_stack([u[:, 0] * d + u[:, 1] * xi, u[:, 1] * eta]))
     q = np.ascontiguousarray(rng.standard_normal(n))
-    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, beta, _cell(pw, cellt), 1e-8)
+    # eps 1e-8: reduced / coarse Bessel tiers; 1e-12: the full tier
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, beta, _cell(pw, cellt), eps)
     s = pw.ParticleSystem(sources=src, targets=src if sym else src.copy(), charges=q)
     culled = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
     monkeypatch.setenv("PWB_NO_CULL", "1")

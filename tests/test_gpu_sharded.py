@@ -122,3 +122,20 @@ def test_sharded_total_field_matches_single_call(pw, gpu):
         outs.append(out.scalar)
     got = torch.cat(outs).cpu().numpy()
     assert rel_l2(got, ref.scalar.cpu().numpy(), gauge=True) <= 1e-13
+
+
+def test_split_rejects_bad_world_sizes(pw, gpu):
+    import torch
+
+    from paper_2111_01083_b200 import configs
+
+    inp = configs.generate("c5", n_src=5000)
+    c = inp.config
+    pz = pw.make_periodizer(c.pde, c.beta, pw.make_unit_cell(*c.cell[:3], c.cell[3]), c.eps)
+    src = torch.from_numpy(inp.sources).cuda()
+    s = pw.ParticleSystem(sources=src, targets=src, charges=torch.from_numpy(inp.charges).cuda())
+    for w in (0, 65):
+        with pytest.raises(pw.PeriwaveError) as e:
+            pw.near_sym_split(pz, s, w)
+        assert e.value.code == pw.ErrorCode.Unsupported
+    assert pw.near_sym_split(pz, s, 1) == [0, pw.near_sym_items(pz, 5000)[0]]
