@@ -33,10 +33,11 @@ F_PAIR = {"c1": 29, "c2": 153, "c3": 48, "c4": 29, "c5": 94}
 F_FAR = {"c1": 70, "c2": 70, "c3": 86, "c4": 70, "c5": 70}
 # fp64-pipe instructions per (target, source) pair-group of the symmetric tile (all images),
 # counted in the SASS of the fast inner loop (cuobjdump; profiles/r1_c4_near_sym_ncu.md)
-# (tools/sass_loop_stats.py), per log tier: the reduced tier runs when eps >= 1e-11 unless
+# (tools/sass_loop_stats.py), per log tier (coarse: 256-entry table log when eps >= 1e-10):
+# the reduced tier runs when eps >= 1e-11 unless
 # PWB_FULL_PRECISION is set (pw_math.cuh log_pos_k)
-FP64_INSTR_PER_GROUP = {("c4", "full"): 29.25, ("c4", "reduced"): 18.25,
-                        ("c3", "full"): 103.0, ("c3", "reduced"): 83.0}
+FP64_INSTR_PER_GROUP = {("c4", "full"): 29.25, ("c4", "reduced"): 18.25, ("c4", "coarse"): 17.25,
+                        ("c3", "full"): 103.0, ("c3", "reduced"): 83.0, ("c3", "coarse"): 82.0}
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_traffic.json")
 
 
@@ -400,6 +401,8 @@ def main():
     # DFMA instruction peak (peak TFLOP/s / 2)
     pipe_frac = None
     tier = "reduced" if (c.eps >= 1e-11 and not os.environ.get("PWB_FULL_PRECISION")) else "full"
+    if tier == "reduced" and c.eps >= 1e-10 and not os.environ.get("PWB_NO_COARSE"):
+        tier = "coarse"  # 256-entry table log (engine.cu a.coarse_log)
     if same and (args.config, tier) in FP64_INSTR_PER_GROUP and not sharded:
         groups = ns * (ns + 1) / 2.0
         pipe_frac = groups * FP64_INSTR_PER_GROUP[(args.config, tier)] / (t_near * 1e-3) / (peak.value * 1e12 / 2.0)

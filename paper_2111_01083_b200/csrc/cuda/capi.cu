@@ -814,7 +814,7 @@ int pwb_nufft_type3(int backend, double eps, size_t n, const double* x, const do
 int pwb_fast_nufft_available(void) { return 1; }
 
 int pwb_eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out) {
-  if (which < 0 || which > 9) return fail_arg("unknown kernel");
+  if (which < 0 || which > 10) return fail_arg("unknown kernel");
   if (n && (!in || !out)) return fail_arg("null argument");
   return guard([&] {
     current_device(-1);

@@ -848,6 +848,9 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
   // coarse Bessel tier of the symmetric screened tile: <= ~1e-11 relative per K0 / K1, three
   // orders below eps >= 1e-9 (c5: eps = 1e-8); PWB_NO_COARSE keeps the reduced tier
   if (a.lowp && pz_.eps >= 1e-9 && std::getenv("PWB_NO_COARSE") == nullptr) a.lowp = 2;
+  // coarse table log of the symmetric Laplace / Stokeslet tiles: <= 9.1e-13 absolute per
+  // pair-log, two orders below eps >= 1e-10 (c4: eps = 1e-10; c3: 1e-8)
+  a.coarse_log = (a.lowp && pz_.eps >= 1e-10 && std::getenv("PWB_NO_COARSE") == nullptr) ? 1 : 0;
   a.cull = std::getenv("PWB_NO_CULL") == nullptr ? 1 : 0;  // A/B and the exactness test only
   if (kind == Kind::Multipole) {
     nk = NearKind::Multipole;

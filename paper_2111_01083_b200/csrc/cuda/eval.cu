@@ -150,6 +150,11 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts<1>(pwk::pw_log_tab_dev_ptr(), 0), bad);
       break;
     }
+    case 10: {  // the coarse table-driven log (256 entries, degree-2 F; eps >= 1e-10)
+      unsigned bad = 0;
+      out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts<1, 8>(pwk::pw_log_tab_dev_ptr<8>(), 0), bad);
+      break;
+    }
     default:
       out[i] = nan("");
   }
@@ -207,7 +212,9 @@ double fp64_peak_probe() {
 
 int eval_in_width(int which) { return (which == 0 || which >= 6) ? 1 : which == 5 ? 4 : 2; }
 int eval_out_width(int which) {
-  return (which <= 1 || which == 8) ? 1 : (which == 3 || which == 4 || which == 9) ? 2 : which == 6 ? 6 : 4;
+  return (which <= 1 || which == 8 || which == 10) ? 1 : (which == 3 || which == 4 || which == 9) ? 2
+                                                      : which == 6                              ? 6
+                                                                                                : 4;
 }
 
 void run_eval(int which, int pde, double beta, int l, size_t n, const double* in_host, double* out_host) {

@@ -119,7 +119,7 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
 // values():      careful per-image semantics (slow path included, sets `flag`);
 // values_fast(): branch-free, only valid when `bad` stays 0 (FAST kernels).
 
-template <bool LOWP_>
+template <bool LOWP_, bool CLOG = false>  // CLOG: coarse table log (eps >= 1e-10, a.coarse_log)
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT,
                        CHUNK = 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
@@ -128,7 +128,8 @@ struct SymLaplace {
   // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
   // blocks per SM fit
-  static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = PWB_SYM_LAPLACE_REPL;
+  static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = CLOG ? 4 : PWB_SYM_LAPLACE_REPL,
+                       LOG_BITS = CLOG ? 8 : pwk::kLogTabBits;  // 256 x 4 x 16 B = 16 KB, 7 blocks still fit
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -181,7 +182,7 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool FAST = false, LOWP = LOWP_;
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
-  static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas;
+  static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
   // mask: bit n * NXI + m set for the images that may hold a pair with beta r < 64 in this
@@ -278,7 +279,7 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
 
 // Stokeslet: V = (log prod r2, Txx, Txy, Tyy [, Px, Py]) with T = sum r r^T / r^2,
 // P = sum r / r^2 (pressurelet, odd).
-template <bool PRESSURE, bool LOWP_>
+template <bool PRESSURE, bool LOWP_, bool CLOG = false>  // CLOG: coarse table log (eps >= 1e-10)
 struct SymStokes {
   // Without pressure the tile carries (a, Txy, b) with a = L/2 - Txx, b = L/2 - Tyy and
   // accumulates the two velocity components directly (u_x ~ a f_x - Txy f_y, u_y ~
@@ -288,7 +289,7 @@ struct SymStokes {
                        TPT = PWB_SYM_STOKES_TPT, CPT = PWB_SYM_STOKES_CPT < PWB_SYM_STOKES_TPT ? PWB_SYM_STOKES_CPT
                                                                                                 : PWB_SYM_STOKES_TPT,
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
-                       LOG_REPL = pwk::kLogTabReplicas;
+                       LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? 8 : pwk::kLogTabBits;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -497,15 +498,15 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   int flag = 0;
   // log constants in registers; the reduced tier's log table in shared memory
   constexpr size_t kTileSmem = sizeof(double) * (static_cast<size_t>(CT) * (2 + K::NW) + kWarps * K::NACC * CT);
-  constexpr int kRepl = K::LOG_REPL;
-  constexpr size_t kTabSmem = sizeof(double2) * pwk::kLogTabEntries * kRepl;
+  constexpr int kRepl = K::LOG_REPL, kBits = K::LOG_BITS;
+  constexpr size_t kTabSmem = sizeof(double2) * (size_t{1} << kBits) * kRepl;
   constexpr bool kTab = K::FAST && K::LOWP && PWB_SYM_LOG_TABLE && kTileSmem + kTabSmem <= 48 * 1024;
-  __shared__ double2 s_lt[kTab ? pwk::kLogTabEntries * kRepl : 1];
-  using LKT = std::conditional_t<kTab, pwk::LogT<kRepl>, pwk::LogK<K::LOWP>>;
+  __shared__ double2 s_lt[kTab ? (1 << kBits) * kRepl : 1];
+  using LKT = std::conditional_t<kTab, pwk::LogT<kRepl, kBits>, pwk::LogK<K::LOWP>>;
   LKT LK;
   if constexpr (kTab) {
-    pwk::log_tab_fill<kRepl>(s_lt, tid, kT);  // visible after the first __syncthreads of the tile loop
-    LK = pwk::log_tab_consts<kRepl>(s_lt, lane);
+    pwk::log_tab_fill<kRepl, kBits>(s_lt, tid, kT);  // visible after the first __syncthreads of the tile loop
+    LK = pwk::log_tab_consts<kRepl, kBits>(s_lt, lane);
   } else if constexpr (K::FAST) {
     LK = pwk::log_consts<K::LOWP>();
   }

@@ -9,6 +9,7 @@ bool launch_stokes(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned l
   if (kind == NearKind::StokesP)
     return a.lowp ? dispatch_sym<SymStokes<true, true>>(a, st, fx, rsd, rsh, r)
                   : dispatch_sym<SymStokes<true, false>>(a, st, fx, rsd, rsh, r);
+  if (a.lowp && a.coarse_log) return dispatch_sym<SymStokes<false, true, true>>(a, st, fx, rsd, rsh, r);
   return a.lowp ? dispatch_sym<SymStokes<false, true>>(a, st, fx, rsd, rsh, r)
                 : dispatch_sym<SymStokes<false, false>>(a, st, fx, rsd, rsh, r);
 }

@@ -54,6 +54,7 @@ struct NearArgs {
   int lowp = 0;                  // near tiles: reduced-precision tier (eps >= 1e-11, pw_math.cuh)
   int cull = 1;                  // screened symmetric tiles: per-tile image mask (near_sym_impl.cuh)
   int unskewed = 0;              // fused layout with shx[n][m] independent of n (xi == 0)
+  int coarse_log = 0;            // symmetric Laplace / Stokeslet tiles: 256-entry table log (eps >= 1e-10)
 };
 
 // ---------------------------------------------------------------- spatial binning (binning.cu)
