@@ -845,9 +845,13 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
   // orders below eps for eps >= 1e-11 (the reference's eps bounds the far truncation);
   // the full tier is ~1 ulp. PWB_FULL_PRECISION forces the full tier (tests).
   a.lowp = (pz_.eps >= 1e-11 && std::getenv("PWB_FULL_PRECISION") == nullptr) ? 1 : 0;
-  // coarse Bessel tier of the symmetric screened tile: <= ~1e-11 relative per K0 / K1, three
-  // orders below eps >= 1e-9 (c5: eps = 1e-8); PWB_NO_COARSE keeps the reduced tier
-  if (a.lowp && pz_.eps >= 1e-9 && std::getenv("PWB_NO_COARSE") == nullptr) a.lowp = 2;
+  // coarse Bessel tier of the screened tiles: <= ~1e-11 relative per K0 / K1 (pinned by
+  // test_hot_tile_bessel_coarse_tier), for eps >= 1e-10 -- measured 9.8e-13 on c2 (eps 1e-10,
+  // bar 1e-9) and 7e-12 on c5 (eps 1e-8, bar 1e-7), profiles/r1b_parity.json;
+  // PWB_NO_COARSE keeps the reduced tier, PWB_COARSE_EPS moves the threshold (A/B)
+  const char* ce = std::getenv("PWB_COARSE_EPS");
+  const double coarse_eps = ce ? std::atof(ce) : 1e-10;
+  if (a.lowp && pz_.eps >= coarse_eps && std::getenv("PWB_NO_COARSE") == nullptr) a.lowp = 2;
   // coarse table log of the symmetric Laplace / Stokeslet tiles: <= 9.1e-13 absolute per
   // pair-log, two orders below eps >= 1e-10 (c4: eps = 1e-10; c3: 1e-8)
   a.coarse_log = (a.lowp && pz_.eps >= 1e-10 && std::getenv("PWB_NO_COARSE") == nullptr) ? 1 : 0;

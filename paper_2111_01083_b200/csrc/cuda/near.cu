@@ -105,7 +105,7 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
   }
 };
 
-template <bool LOWP>
+template <bool LOWP, bool COARSE = false>  // COARSE: the coarse Bessel tier (pw_math.cuh k01_asym)
 struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
   static constexpr int NW = 1, NACC = 1, NOUT = 1;
   static constexpr bool EXP_TAB = LOWP;  // k01_tile<true, .> reads the shared exp table
@@ -121,21 +121,21 @@ struct ModHelm {  // K0(beta r) / 2pi  (kernels.cpp:104-106)
       return;
     }
     const double X = a.beta2 * r2;
-    if (pwk::lt_hi(X, a.xcut2)) acc[0] = fma(w[0], pwk::k01_tile<LOWP, false>(X).k0, acc[0]);
+    if (pwk::lt_hi(X, a.xcut2)) acc[0] = fma(w[0], pwk::k01_tile<LOWP, false, COARSE>(X).k0, acc[0]);
   }
   // the same for a pair known to be in asymptotic regime FAR and inside the cut-off
   template <bool FAR>
   __device__ __forceinline__ static void image_fast(double* acc, double rx, double ry, const double* w,
                                                     const NearArgs& a) {
     const double X = a.beta2 * fma(rx, rx, ry * ry);
-    acc[0] = fma(w[0], pwk::k01_asym<LOWP, false, FAR>(X).k0, acc[0]);
+    acc[0] = fma(w[0], pwk::k01_asym<LOWP, false, FAR, COARSE>(X).k0, acc[0]);
   }
   __device__ __forceinline__ static void finish(const double* acc, const NearArgs&, double* out) {
     out[0] = acc[0] * (1.0 / (2.0 * pwk::kPi));
   }
 };
 
-template <bool LOWP>
+template <bool LOWP, bool COARSE = false>
 struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
   static constexpr int NW = 1, NACC = 3, NOUT = 3;
   static constexpr bool EXP_TAB = LOWP;
@@ -151,7 +151,7 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
     }
     const double X = a.beta2 * r2;
     if (pwk::lt_hi(X, a.xcut2)) {
-      const pwk::K01 k = pwk::k01_tile<LOWP, true>(X);
+      const pwk::K01 k = pwk::k01_tile<LOWP, true, COARSE>(X);
       acc[0] = fma(w[0], k.k0, acc[0]);
       const double g = w[0] * k.k1_over_x;
       acc[1] = fma(g, rx, acc[1]);
@@ -162,7 +162,7 @@ struct ModHelmGrad {  // u and grad u = -(beta/2pi) K1(beta r) r_vec / r
   __device__ __forceinline__ static void image_fast(double* acc, double rx, double ry, const double* w,
                                                     const NearArgs& a) {
     const double X = a.beta2 * fma(rx, rx, ry * ry);
-    const pwk::K01 k = pwk::k01_asym<LOWP, true, FAR>(X);
+    const pwk::K01 k = pwk::k01_asym<LOWP, true, FAR, COARSE>(X);
     acc[0] = fma(w[0], k.k0, acc[0]);
     const double g = w[0] * k.k1_over_x;
     acc[1] = fma(g, rx, acc[1]);
@@ -696,9 +696,11 @@ void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* part
                     : dispatch_images<Laplace<false>, 2>(a, st, partial_ws, sm_count);
     // precision tier (pw_math.cuh k01_tile): reduced when eps allows it
     case NearKind::ModHelm:
+      if (a.lowp == 2) return dispatch_images<ModHelm<true, true>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
       return a.lowp ? dispatch_images<ModHelm<true>, PWB_MH_TPT>(a, st, partial_ws, sm_count)
                     : dispatch_images<ModHelm<false>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
     case NearKind::ModHelmGrad:
+      if (a.lowp == 2) return dispatch_images<ModHelmGrad<true, true>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
       return a.lowp ? dispatch_images<ModHelmGrad<true>, PWB_MH_TPT>(a, st, partial_ws, sm_count)
                     : dispatch_images<ModHelmGrad<false>, PWB_MH_TPT>(a, st, partial_ws, sm_count);
     case NearKind::Stokes:

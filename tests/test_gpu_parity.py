@@ -162,8 +162,10 @@ def test_near_and_far_vs_reference(pw, gpu, ref, case, pressure):
             err = rel_l2(got.scalar, want["scalar"], gauge and mode == 1)
         else:
             err = rel_l2(got.velocity, want["velocity"], gauge and mode == 1)
-        # near images: ~1 ulp kernels, or the reduced tier when eps >= 1e-11 (pw_math.cuh)
-        near_tol = max(1e-13, 1e-4 * eps)
+        # near images: ~1 ulp kernels, the reduced tier when eps >= 1e-11, and for the
+        # modified-Helmholtz kernels the coarse Bessel tier (<= ~1e-11 relative per K0 / K1)
+        # when eps >= 1e-10 (pw_math.cuh, engine.cu)
+        near_tol = 1e-11 if (pde == 1 and eps >= 1e-10) else max(1e-13, 1e-4 * eps)
         tol = 10 * eps if mode == 1 else near_tol
         assert err <= tol, (name, mode, err)
         if pressure:
