@@ -89,6 +89,9 @@ namespace sym {
 #ifndef PWB_SYM_STOKES_MINB
 #define PWB_SYM_STOKES_MINB 0  // 0: ptxas's own register allocation (166 registers, 3 blocks/SM)
 #endif
+#ifndef PWB_SYM_KEEP_SMEM
+#define PWB_SYM_KEEP_SMEM 0  // 1: the fast path's pre-tile row sums live in shared memory (frees registers)
+#endif
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 7  // 7 x 4 warps/SM at 72 registers (128-point column tiles leave room in shared memory): c4 667 -> 653 ms vs 6
 #endif
@@ -465,6 +468,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   const NearArgs& a = S.a;
   __shared__ double s_x[CT], s_y[CT], s_w[K::NW][CT];
   __shared__ double s_col[kWarps][K::NACC][CT];
+  __shared__ double s_keep[PWB_SYM_KEEP_SMEM && K::FAST ? TPT * K::NACC : 1][PWB_SYM_KEEP_SMEM && K::FAST ? kT : 1];
 
   // work item -> (row tile I, first column tile)
   const int item = S.item0 + static_cast<int>(blockIdx.x);
@@ -646,11 +650,18 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       careful = false;
     }
     if (K::FAST) {
-      double keep[TPT][K::NACC];
+      // the row sums before this tile, for the careful redo: in shared memory (each thread
+      // its own column, no sync needed) when PWB_SYM_KEEP_SMEM, else in registers
+      double keep[PWB_SYM_KEEP_SMEM ? 1 : TPT][K::NACC];
 #pragma unroll
       for (int k = 0; k < TPT; ++k)
 #pragma unroll
-        for (int c = 0; c < K::NACC; ++c) keep[k][c] = racc[k][c];
+        for (int c = 0; c < K::NACC; ++c) {
+          if constexpr (PWB_SYM_KEEP_SMEM)
+            s_keep[k * K::NACC + c][tid] = racc[k][c];
+          else
+            keep[k][c] = racc[k][c];
+        }
       std::conditional_t<kTab, unsigned, int> bad = 0;  // see pwk::log_bad
 #pragma unroll K::UNROLL
       for (int i = 0; i < CT; ++i) {
@@ -677,7 +688,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int k = 0; k < TPT; ++k)
 #pragma unroll
-          for (int c = 0; c < K::NACC; ++c) racc[k][c] = keep[k][c];
+          for (int c = 0; c < K::NACC; ++c) racc[k][c] = PWB_SYM_KEEP_SMEM ? s_keep[k * K::NACC + c][tid] : keep[k][c];
         for (int i = tid; i < CT; i += kT)
 #pragma unroll
           for (int c = 0; c < K::NACC; ++c)
