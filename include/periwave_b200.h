@@ -206,10 +206,18 @@ int pwb_far_target_pass(const pwb_periodizer* pz, const pwb_system* sys, const p
  * n * nout * 3 int64, target-major: acc[(l*nout + c)*3 + limb]); the accumulators
  * are summed exactly as integers (e.g. ncclReduceScatter(ncclInt64, sum) so each
  * rank receives a contiguous slice of targets), and pwb_fixed_to_field adds a
- * slice into the outputs. Bitwise deterministic for any split. */
+ * slice into the outputs. Bitwise deterministic for any split.
+ * The accumulator holds the near field times 2^scale_exp (*scale_exp, written by
+ * pwb_near_sym_partial; derived from max |strength| and n, hence identical on every rank
+ * that holds the same strengths): pass it to pwb_fixed_to_field.
+ * *status: bit 0 = a non-identity exact coincidence (the reference's
+ * CoincidentSourceTarget, apply.cpp:544-545), bit 1 = the fixed-point range was exceeded
+ * (non-finite strengths). The call does NOT raise these (returns PWB_OK), so that every
+ * rank can combine the status words (e.g. allreduce MAX) before the reduce-scatter and
+ * raise the same error everywhere instead of leaving peers blocked in a collective. */
 int pwb_near_sym_items(const pwb_periodizer* pz, size_t n, const pwb_options* opt, long* n_items, int* nout);
 int pwb_near_sym_partial(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, long item_begin,
-                         long item_end, int64_t* acc);
+                         long item_end, int64_t* acc, int* scale_exp, int* status);
 /* Item boundaries bounds[0..world] (host array of world + 1, world <= 64) of a balanced split of
  * the symmetric work items over `world` ranks: rank r runs [bounds[r], bounds[r+1]). For the
  * screened kernels (modified Helmholtz) the split balances the estimated cost per item from
@@ -219,7 +227,7 @@ int pwb_near_sym_partial(const pwb_periodizer* pz, const pwb_system* sys, const 
 int pwb_near_sym_split(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, int world,
                        long* bounds);
 int pwb_fixed_to_field(const pwb_periodizer* pz, const pwb_options* opt, const int64_t* acc, size_t n_targets,
-                       pwb_field* out);
+                       int scale_exp, pwb_field* out);
 /* Strength/neutrality/cell checks of apply_far (proj/src/apply.cpp:350-393, cell.cpp:77-94),
  * evaluated on the device for device-resident systems. */
 int pwb_validate(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt);

@@ -504,3 +504,15 @@ void port_nufft_type3(size_t n, const double* x, const double* c, size_t nk, con
     f[2 * k + 1] = im;
   }
 }
+
+/* xorshift64* step mapped to [0, 1), restating proj/include/periwave/util.hpp:83-98
+   (seed 0 is replaced by the golden-ratio constant, as upstream). */
+void port_rng_uniform(unsigned long long seed, size_t n, double* out) {
+  unsigned long long s = seed ? seed : 0x9e3779b97f4a7c15ull;
+  for (size_t i = 0; i < n; ++i) {
+    s ^= s >> 12;
+    s ^= s << 25;
+    s ^= s >> 27;
+    out[i] = (double)((s * 0x2545f4914f6cdd1dull) >> 11) * 0x1.0p-53;
+  }
+}

@@ -19,6 +19,8 @@ enum { PORT_LAPLACE = 0, PORT_MODHELM = 1, PORT_STOKES = 2, PORT_MODSTOKES = 3, 
 
 /* modified Bessel K_l(x), own evaluation (series / trapezoidal integral) */
 double port_bessel_kn(int l, double x);
+/* xorshift64* uniform stream of the reference Rng (proj/include/periwave/util.hpp:83-98). */
+void port_rng_uniform(unsigned long long seed, size_t n, double* out);
 
 /* Near images: out += sum_img sum_j G((t_l - s_j) - shift_img) w_j, with the
  * reference's exact-zero rules (apply.cpp:481-546). Output per target:

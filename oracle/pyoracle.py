@@ -26,6 +26,18 @@ def _p(a):
     return None if a is None else np.ascontiguousarray(a, dtype=np.float64).ctypes.data
 
 
+_rng_src = None
+
+
+def rng_uniform(seed: int, n: int) -> np.ndarray:
+    """The reference's Rng::uniform stream from the checkers, never the product library:
+    oracle/_ref's own periwave::Rng, else the C restatement in oracle/port."""
+    global _rng_src
+    if _rng_src is None:
+        _rng_src = Ref() if ref_available() else Port()
+    return _rng_src.rng_uniform(seed, n)
+
+
 class RefError(RuntimeError):
     def __init__(self, status, msg):
         self.status = status
@@ -76,7 +88,13 @@ class Ref:
         L.ref_sommerfeld_rule.argtypes = [_i, _d, _d, _d, _d, _i, _d, _d, _sz, _vp, _vp, ctypes.POINTER(_sz), _vp, _vp]
         L.ref_interp_coeffs.argtypes = [_d, _d, _i, _d, _vp]
         L.ref_unit_cell_m0.argtypes = [_d, _d, _d, _i, ctypes.POINTER(_i)]
+        L.ref_rng_uniform.argtypes = [ctypes.c_ulonglong, _sz, _vp]
         self.L = L
+
+    def rng_uniform(self, seed, n):
+        out = np.empty(n, dtype=np.float64)
+        self.L.ref_rng_uniform(int(seed), int(n), out.ctypes.data)
+        return out
 
     def _chk(self, st):
         if st != 0:
@@ -312,7 +330,13 @@ class Port:
         L.port_nufft_type1.argtypes = [_sz, _vp, _vp, _sz, _vp]
         L.port_nufft_type2.argtypes = [_sz, _vp, _sz, _vp, _vp]
         L.port_nufft_type3.argtypes = [_sz, _vp, _vp, _sz, _vp, _vp]
+        L.port_rng_uniform.argtypes = [ctypes.c_ulonglong, _sz, _vp]
         self.L = L
+
+    def rng_uniform(self, seed, n):
+        out = np.empty(n, dtype=np.float64)
+        self.L.port_rng_uniform(int(seed), int(n), out.ctypes.data)
+        return out
 
     def bessel_kn(self, l, x):
         return self.L.port_bessel_kn(int(l), float(x))

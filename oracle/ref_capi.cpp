@@ -136,6 +136,13 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// The reference's own periwave::Rng stream (util.hpp:83-98): the bench's reference arm
+// draws its inputs from it, so that arm never loads the product library.
+void ref_rng_uniform(unsigned long long seed, size_t n, double* out) {
+  periwave::Rng r(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = r.uniform();
+}
+
 int ref_unit_cell_m0(double d, double xi, double eta, int periodicity, int* m0) {
   return guarded([&] { *m0 = cell_of(d, xi, eta, periodicity).m0; });
 }

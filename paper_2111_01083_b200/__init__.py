@@ -189,10 +189,10 @@ def lib() -> ctypes.CDLL:
     L.pwb_near_sym_items.argtypes = [vp, sz, ctypes.POINTER(_Options), ctypes.POINTER(ctypes.c_long),
                                      ctypes.POINTER(i)]
     L.pwb_near_sym_partial.argtypes = [vp, ctypes.POINTER(_System), ctypes.POINTER(_Options), ctypes.c_long,
-                                       ctypes.c_long, vp]
+                                       ctypes.c_long, vp, ctypes.POINTER(i), ctypes.POINTER(i)]
     L.pwb_near_sym_split.argtypes = [vp, ctypes.POINTER(_System), ctypes.POINTER(_Options), i,
                                      ctypes.POINTER(ctypes.c_long)]
-    L.pwb_fixed_to_field.argtypes = [vp, ctypes.POINTER(_Options), vp, sz, ctypes.POINTER(_Field)]
+    L.pwb_fixed_to_field.argtypes = [vp, ctypes.POINTER(_Options), vp, sz, i, ctypes.POINTER(_Field)]
     L.pwb_brute_force_far.argtypes = [vp, ctypes.POINTER(_System), i, ctypes.POINTER(_Options),
                                       ctypes.POINTER(_Field)]
     L.pwb_periodicity_residual.argtypes = [vp, ctypes.POINTER(_System), i, ctypes.POINTER(_Options),
@@ -671,16 +671,37 @@ def near_sym_items(pz: Periodizer, n: int, opt: Optional[ApplyOptions] = None):
     return items.value, nout.value
 
 
+# status bits of near_sym_partial (include/periwave_b200.h)
+SYM_COINCIDENT = 1
+SYM_OVERFLOW = 2
+
+
 def near_sym_partial(pz: Periodizer, sys: ParticleSystem, acc, item_begin: int, item_end: int,
-                     opt: Optional[ApplyOptions] = None) -> None:
+                     opt: Optional[ApplyOptions] = None):
     """Adds work items [begin, end) of the symmetric near field into the int64 accumulator
-    `acc` (device, n * nout * 3, target-major). sys.targets must be sys.sources."""
+    `acc` (device, n * nout * 3, target-major). sys.targets must be sys.sources.
+
+    Returns (scale_exp, status): the accumulator holds the field times 2**scale_exp (pass
+    it to fixed_to_field); status bit SYM_COINCIDENT / SYM_OVERFLOW is NOT raised here, so
+    the ranks can agree on it before the reduce-scatter (raise_sym_status)."""
     s, mem = sys._c()
     if mem != MEM_DEVICE:
         raise ValueError("near_sym_partial takes device tensors")
     o = (opt or ApplyOptions())._c()
+    k, st = ctypes.c_int(0), ctypes.c_int(0)
     _check(lib().pwb_near_sym_partial(pz.handle, ctypes.byref(s), ctypes.byref(o), item_begin, item_end,
-                                      acc.data_ptr()))
+                                      acc.data_ptr(), ctypes.byref(k), ctypes.byref(st)))
+    return k.value, st.value
+
+
+def raise_sym_status(status: int) -> None:
+    """The error the reference raises for a combined near_sym_partial status word."""
+    if status & SYM_COINCIDENT:  # apply.cpp:544-545
+        raise PeriwaveError(1 + ErrorCode.CoincidentSourceTarget,
+                            "a target coincides with a lattice image of a source")
+    if status & SYM_OVERFLOW:
+        raise PeriwaveError(1 + ErrorCode.Unsupported,
+                            "symmetric near field: strengths or kernel values exceed the fixed-point range")
 
 
 def near_sym_split(pz: Periodizer, sys: ParticleSystem, world: int, opt: Optional[ApplyOptions] = None):
@@ -696,12 +717,13 @@ def near_sym_split(pz: Periodizer, sys: ParticleSystem, world: int, opt: Optiona
 
 
 def fixed_to_field(pz: Periodizer, acc, n_targets: int, out: FieldResult, opt: Optional[ApplyOptions] = None,
-                   like=None) -> FieldResult:
-    """out += the fp64 value of a fixed-point accumulator slice (device)."""
+                   like=None, scale_exp: int = 0) -> FieldResult:
+    """out += 2**-scale_exp times the fp64 value of a fixed-point accumulator slice (device)."""
     opt = opt or ApplyOptions()
     res, f = _field_for(pz, opt, n_targets, True, like if like is not None else acc, out)
     o = opt._c()
-    _check(lib().pwb_fixed_to_field(pz.handle, ctypes.byref(o), acc.data_ptr(), n_targets, ctypes.byref(f)))
+    _check(lib().pwb_fixed_to_field(pz.handle, ctypes.byref(o), acc.data_ptr(), n_targets, int(scale_exp),
+                                    ctypes.byref(f)))
     return res
 
 

@@ -735,8 +735,8 @@ int pwb_near_sym_items(const pwb_periodizer* h, size_t n, const pwb_options* o, 
 }
 
 int pwb_near_sym_partial(const pwb_periodizer* h, const pwb_system* s, const pwb_options* o, long item_begin,
-                         long item_end, int64_t* acc) {
-  if (!h || !s || !acc) return fail_arg("null argument");
+                         long item_end, int64_t* acc, int* scale_exp, int* status) {
+  if (!h || !s || !acc || !scale_exp || !status) return fail_arg("null argument");
   if (s->memory != PWB_MEM_DEVICE) return fail_arg("sharded passes take device memory");
   return guard([&] {
     const int dev = current_device(o ? o->device : -1);
@@ -746,7 +746,7 @@ int pwb_near_sym_partial(const pwb_periodizer* h, const pwb_system* s, const pwb
     pwb::DevSys ds;
     stage_in(p, s, p.stream_for(opt), &ds);
     p.validate(ds, opt, false, /*neutrality=*/true);
-    p.sym_partial(ds, opt, item_begin, item_end, reinterpret_cast<unsigned long long*>(acc));
+    *status = p.sym_partial(ds, opt, item_begin, item_end, reinterpret_cast<unsigned long long*>(acc), scale_exp);
     return OK;
   });
 }
@@ -767,7 +767,8 @@ int pwb_near_sym_split(const pwb_periodizer* h, const pwb_system* s, const pwb_o
   });
 }
 
-int pwb_fixed_to_field(const pwb_periodizer* h, const pwb_options* o, const int64_t* acc, size_t n, pwb_field* f) {
+int pwb_fixed_to_field(const pwb_periodizer* h, const pwb_options* o, const int64_t* acc, size_t n, int scale_exp,
+                       pwb_field* f) {
   if (!h || !acc || !f) return fail_arg("null argument");
   if (f->memory != PWB_MEM_DEVICE) return fail_arg("fixed-point conversion takes device memory");
   return guard([&] {
@@ -777,7 +778,7 @@ int pwb_fixed_to_field(const pwb_periodizer* h, const pwb_options* o, const int6
     pwb::Opts opt = opts_from(o);
     pwb::DevOut dout;
     stage_out(p, f, n, p.stream_for(opt), false, &dout);
-    p.fixed_finish(opt, reinterpret_cast<const unsigned long long*>(acc), n, dout);
+    p.fixed_finish(opt, reinterpret_cast<const unsigned long long*>(acc), n, scale_exp, dout);
     return OK;
   });
 }

@@ -166,6 +166,9 @@ Plan::Plan(const periwave::Periodizer& pz, int device) : pz_(pz), device_(device
 }
 
 Plan::~Plan() {
+  if (cudaGetDevice(&restore_.prev) != cudaSuccess) restore_.prev = -1;
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);  // nothing in flight when the FFT plans and buffers go
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
@@ -594,7 +597,7 @@ void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::
       a.cplx = f.ws == WeightSet::Coef ? 1 : 0;
       double* grid = nu_grid_.as<double>(static_cast<size_t>(va_.mg) * va_.nf * 2);
       launch_spread(a, grid, nu_partial_, sms_, st);
-      fft_lines(grid, va_.nf, va_.mg, +1, st);
+      fft_.exec(grid, va_.nf, va_.mg, +1, st);
       launch_deconv(grid, va_.mg, va_.nf, va_.nmodes, static_cast<const double*>(va_.fac.get()), coeff + off, st);
       off += static_cast<size_t>(va_.mg) * va_.nmodes * 2;
       continue;
@@ -808,7 +811,7 @@ bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
         launch_mix(ma, coeff + off, G, st);
         double* grid = nu_grid_.as<double>(static_cast<size_t>(va_.mg) * va_.nf * 2);
         launch_precorrect(G, va_.mg, va_.nf, va_.nmodes, static_cast<const double*>(va_.fac.get()), grid, st);
-        fft_lines(grid, va_.nf, va_.mg, -1, st);
+        fft_.exec(grid, va_.nf, va_.mg, -1, st);
         const SpreadArgs a = vert_spread_args(s, false);
         launch_interp(a, grid, kind == Kind::Multipole ? nullptr : out.scalar,
                       kind == Kind::Multipole ? out.complex_scalar : nullptr, true, st);
@@ -978,8 +981,8 @@ void Plan::sym_split(const DevSys& s, const Opts& o, int world, long* bounds) {
   cudaStream_t st = stream_for(o);
   bin_inputs(s, a, st);  // the same sorted points sym_partial runs on
   const size_t nb = near_sym_tiles(s.nt);
-  int* rs_dev = sym_rows_.as<int>(nb + 1);
-  int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
+  auto* rs_dev = sym_rows_.as<long long>(nb + 1);
+  auto* rs_host = static_cast<long long*>(sym_rows_host_.ensure((nb + 1) * sizeof(long long)));
   const size_t bytes = near_sym_split_bytes(s.nt, items);
   void* ws = sym_split_ws_.ensure(bytes);
   long* hb = static_cast<long*>(host_checks_.ensure(65 * sizeof(long)));
@@ -992,7 +995,8 @@ int Plan::near_nout(const Opts& o) const {
   return static_cast<int>(near_outputs(near_args(DevSys{}, o, DevOut{}, false, 0, 0, false, a)));
 }
 
-void Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc) {
+int Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc,
+                      int* scale_exp) {
   require(s.tgt == s.src && s.nt == s.ns, ErrorCode::Unsupported,
           "the symmetric near field needs the sources as targets");
   cudaStream_t st = stream_for(o);
@@ -1002,9 +1006,14 @@ void Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, uns
   int* flag = flag_.as<int>(1);
   cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
   a.flag = flag;
+  // the fixed-point scale comes from the global strengths (every rank holds all of them,
+  // so every rank scales identically and the integer reduce-scatter stays exact)
+  unsigned* maxhi = fx_maxhi_.as<unsigned>(1);
+  launch_fx_maxhi(a, maxhi, st);
+  a.fx_maxhi = maxhi;
   const size_t nb = near_sym_tiles(s.nt);
-  int* rs_dev = sym_rows_.as<int>(nb + 1);
-  int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
+  auto* rs_dev = sym_rows_.as<long long>(nb + 1);
+  auto* rs_host = static_cast<long long*>(sym_rows_host_.ensure((nb + 1) * sizeof(long long)));
   SymRange r;
   r.begin = begin;
   r.end = end;
@@ -1030,16 +1039,19 @@ void Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, uns
   cuda_check(cudaEventRecord(ev_[3], st), "event");
   near_timed_ = true;
   cuda_check(cudaGetLastError(), "near launch");
-  int* hflag = static_cast<int*>(host_checks_.ensure(64 * sizeof(double)));
-  cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+  auto* h = static_cast<unsigned*>(host_checks_.ensure(64 * sizeof(double)));
+  cuda_check(cudaMemcpyAsync(h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+  cuda_check(cudaMemcpyAsync(h + 1, maxhi, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H maxhi");
   cuda_check(cudaStreamSynchronize(st), "near sync");
-  require(*hflag == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
+  if (scale_exp) *scale_exp = fx_exponent(h[1], s.ns);
+  return static_cast<int>(h[0]);
 }
 
-void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, const DevOut& out) {
+void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, int scale_exp, const DevOut& out) {
+  require(scale_exp >= -960 && scale_exp <= 960, ErrorCode::Unsupported, "fixed-point scale exponent out of range");
   NearArgs a;
   near_args(DevSys{}, o, out, false, 0, 0, false, a);
-  launch_fx_finish(acc, n, a.out0, a.nout0, a.out1, a.nout1, nullptr, stream_for(o));
+  launch_fx_finish(acc, n, a.out0, a.nout0, a.out1, a.nout1, nullptr, nullptr, 0, scale_exp, nullptr, stream_for(o));
   cuda_check(cudaGetLastError(), "fixed-point finish");
   cuda_check(cudaStreamSynchronize(stream_for(o)), "sync");
 }
@@ -1118,8 +1130,11 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   if (symmetric) {
     const size_t nb = near_sym_tiles(s.nt);
     auto* fx = sym_fx_.as<unsigned long long>(3 * s.nt * nout);
-    int* rs_dev = sym_rows_.as<int>(nb + 1);
-    int* rs_host = static_cast<int*>(sym_rows_host_.ensure((nb + 1) * sizeof(int)));
+    auto* rs_dev = sym_rows_.as<long long>(nb + 1);
+    auto* rs_host = static_cast<long long*>(sym_rows_host_.ensure((nb + 1) * sizeof(long long)));
+    unsigned* maxhi = fx_maxhi_.as<unsigned>(1);
+    launch_fx_maxhi(a, maxhi, st);
+    a.fx_maxhi = maxhi;
     done = launch_near_sym(nk, a, st, fx, rs_dev, rs_host, SymRange{});
   }
   if (!done) {
@@ -1132,7 +1147,20 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   int* hflag = static_cast<int*>(host_checks_.ensure(64 * sizeof(double)));
   cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
   cuda_check(cudaStreamSynchronize(st), "near sync");
-  require(*hflag == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
+  require((*hflag & 1) == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
+  if (*hflag & 2) {
+    // a scaled partial sum left the fixed-point range (non-finite strengths, or kernel
+    // values beyond ~2^60 times the strengths): the readout was skipped; redo the near
+    // field on the one-sided tile, which sums in fp64 like the reference
+    cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
+    double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
+    launch_near(nk, a, st, ws, sms_);
+    cuda_check(cudaEventRecord(ev_[3], st), "event");
+    cuda_check(cudaGetLastError(), "near launch");
+    cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+    cuda_check(cudaStreamSynchronize(st), "near sync");
+    require((*hflag & 1) == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
+  }
 }
 
 bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {

@@ -3,14 +3,33 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "periwave/periwave.hpp"
 #include "pw_engine.cuh"
 
 namespace pwb {
+
+// cuFFT plans of one owner (a device Plan, or one standalone transform call), keyed by
+// (nf, lines): every owner has its own handles and work areas, made on the owner's
+// device, so two Plans (two devices, or two streams in two threads) never share a work
+// area; the handles are destroyed with their owner (nufft.cu).
+class FftPlans {
+ public:
+  FftPlans() = default;
+  FftPlans(const FftPlans&) = delete;
+  FftPlans& operator=(const FftPlans&) = delete;
+  ~FftPlans();
+  // batched in-place complex transform of `lines` lines of nf points; sign +1 = e^{+i}
+  void exec(double* data, int nf, int lines, int sign, cudaStream_t st);
+
+ private:
+  std::map<std::pair<int, int>, int> plans_;  // cufftHandle is an int
+};
 
 // RAII device buffer that only grows.
 class DevBuf {
@@ -159,10 +178,13 @@ class Plan {
   // points, a range of them into a fixed-point accumulator, and its conversion
   long sym_items(const Opts& o, size_t n);
   int near_nout(const Opts& o) const;
-  void sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc);
+  // returns status bits (1: coincidence, 2: fixed-point range exceeded) instead of throwing,
+  // so every rank can agree on the error before a collective; *scale_exp = the exponent k
+  // of the fixed-point scale (fx_exponent) the accumulator is in
+  int sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsigned long long* acc, int* scale_exp);
   // item boundaries [world + 1] of a balanced multi-GPU split of the symmetric items
   void sym_split(const DevSys& s, const Opts& o, int world, long* bounds);
-  void fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, const DevOut& out);
+  void fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, int scale_exp, const DevOut& out);
   // full pipeline on device pointers; returns the accelerated flag
   bool total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images);
 
@@ -175,6 +197,14 @@ class Plan {
   PinnedBuf pin;
 
  private:
+  // declared first, destroyed last: ~Plan makes the plan's device current for the member
+  // destructors (cuFFT handles, device buffers) and this restores the caller's device
+  struct RestoreDevice {
+    int prev = -1;
+    ~RestoreDevice() {
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+  } restore_;
   const periwave::Periodizer& pz_;
   int device_ = 0;
   int sms_ = 148;
@@ -182,7 +212,7 @@ class Plan {
   std::vector<std::unique_ptr<Family>> fams_;
   DevBuf s2pw_partial_, coeff_ws_, A_, B_, m0_, near_partial_, flag_, red_m_, red_c_, red_out_;
   PinnedBuf host_checks_;
-  DevBuf sym_fx_, sym_rows_, sym_split_ws_;
+  DevBuf sym_fx_, sym_rows_, sym_split_ws_, fx_maxhi_;
   PinnedBuf sym_rows_host_;
   // spatially binned copies of the near-field inputs (binning.cu)
   DevBuf bin_ws_, bin_perm_s_, bin_perm_t_, bin_src_, bin_tgt_, bin_q_, bin_vec_, bin_nrm_;
@@ -194,6 +224,7 @@ class Plan {
   VertAccel va_;
   HorizAccel ha_;
   DevBuf nu_grid_, nu_partial_, nu_lines_;
+  FftPlans fft_;  // this plan's own cuFFT handles (its device, its work areas)
   bool horiz_accel(const Family& f, const Opts& o, periwave::ApplyPath path) const;
   void ensure_horiz_accel(double inner_eps);
   size_t horiz_coeff_len() const;

@@ -616,13 +616,14 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   // split count chosen so the last wave is as full as possible (ncu r1, c2: 782
   // blocks on 592 slots left the second wave 32 % occupied, fp64 pipe 61 %).
   // Each split keeps >= 16 sources (c1: 1000 x 1000 runs 4 target blocks x 63 splits).
-  static int resident = 0;  // per instantiation: blocks per SM at this kernel's registers/smem
-  if (resident == 0) {
+  // per instantiation: blocks per SM at this kernel's registers/smem (thread-safe static
+  // init; the value depends only on the kernel and the sm_100a target, not the device)
+  static const int resident = [] {
     int r = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, near_tile_kernel<KER, NXI, NROW, TPT>, kThreads, 0),
                "occupancy");
-    resident = r > 0 ? r : 1;
-  }
+    return r > 0 ? r : 1;
+  }();
   const size_t slots = static_cast<size_t>(sm_count) * resident;
   int splits = 1;
   if (partial_ws != nullptr && bx < 8 * slots) {

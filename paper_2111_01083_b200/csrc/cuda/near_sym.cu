@@ -6,14 +6,21 @@
 
 #include <cub/device/device_scan.cuh>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace pwb {
 namespace {
 
 __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double* out0, int nout0, double* out1,
-                                 int nout1, const int* out_row) {
+                                 int nout1, const int* out_row, const unsigned* maxhi, size_t n_src, int k_host,
+                                 const int* flag) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int nout = nout0 + nout1;
   if (i >= n * nout) return;
+  if (flag && (*flag & 2)) return;  // fixed-point range exceeded: the engine redoes the near field in fp64
+  const double inv = fx_scale(-(maxhi ? fx_exponent(*maxhi, n_src) : k_host));
   const long long a = static_cast<long long>(acc[3 * i]);
   const long long b = static_cast<long long>(acc[3 * i + 1]);
   const long long c = static_cast<long long>(acc[3 * i + 2]);
@@ -22,18 +29,61 @@ __global__ void fx_finish_kernel(const unsigned long long* acc, size_t n, double
   const size_t l = out_row ? static_cast<size_t>(out_row[i / nout]) : i / nout;
   const int k = static_cast<int>(i % nout);
   double* dst = k < nout0 ? out0 + l * nout0 + k : out1 + l * nout1 + (k - nout0);
-  *dst += v;
+  *dst += v * inv;  // exact power-of-two rescale
+}
+
+// high word of max |w| over the strengths (q, or both force components); the high
+// words of non-negative doubles order like the values, so an integer atomicMax is an
+// exact, order-independent max (NaN / inf land above 0x7ff00000)
+__global__ void fx_maxhi_kernel(const double* q, const double2* vec, size_t n, unsigned* maxhi) {
+  unsigned m = 0u;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
+    if (q) m = max(m, static_cast<unsigned>(__double2hiint(q[j])) & 0x7fffffffu);
+    if (vec) {
+      const double2 f = vec[j];
+      m = max(m, static_cast<unsigned>(__double2hiint(f.x)) & 0x7fffffffu);
+      m = max(m, static_cast<unsigned>(__double2hiint(f.y)) & 0x7fffffffu);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(maxhi, m);
 }
 
 }  // namespace
 
 void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int nout0, double* out1, int nout1,
-                      const int* out_row, cudaStream_t st) {
+                      const int* out_row, const unsigned* maxhi_dev, size_t n_src, int k_host, const int* flag,
+                      cudaStream_t st) {
   const size_t total = n * static_cast<size_t>(nout0 + nout1);
   if (total == 0) return;
   fx_finish_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(fx, n, out0, nout0, out1, nout1,
-                                                                               out_row);
+                                                                               out_row, maxhi_dev, n_src, k_host, flag);
   count_launches(1);
+}
+
+void launch_fx_maxhi(const NearArgs& a, unsigned* maxhi, cudaStream_t st) {
+  cuda_check(cudaMemsetAsync(maxhi, 0, sizeof(unsigned), st), "memset maxhi");
+  if (a.ns == 0) return;
+  const size_t blocks = std::min<size_t>((a.ns + 255) / 256, 4 * 148);
+  fx_maxhi_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a.q, a.vec, a.ns, maxhi);
+  count_launches(1);
+}
+
+void set_max_carveout(const void* kernel) {
+  // Static shared memory (tile + per-warp column partials) is what limits residency next
+  // to registers: ask for the maximum carveout so registers decide (ncu r1: the default
+  // carveout capped SymLaplace at 5 blocks on shared memory alone). Per device: a second
+  // device in the same process gets its own attribute call.
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "get device");
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert({dev, kernel}).second) return;
+  cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+             "smem carveout");
 }
 
 // upper bound on the number of row tiles (the smallest row tile is 128 points)
@@ -78,7 +128,7 @@ __global__ void tile_box_kernel(const double2* __restrict__ p, size_t n, int til
 // Estimated cost of every work item (row tile I, column tiles J0..J1): per tile pair a
 // staging overhead plus, per image, what the tile will do with it (near_sym_impl.cuh):
 // nothing when masked, a branch-free regime sweep, or the per-pair dispatch.
-__global__ void item_cost_kernel(const double* __restrict__ box, const int* __restrict__ row_start, int nb, int chunk,
+__global__ void item_cost_kernel(const double* __restrict__ box, const long long* __restrict__ row_start, int nb, int chunk,
                                  long items, const NearArgs a, float* __restrict__ cost) {
   const long item = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= items) return;
@@ -166,23 +216,23 @@ void near_sym_shape(NearKind kind, int* tile, int* chunk) {
 size_t near_sym_split_bytes(size_t n, long items) {
   size_t tmp = 0;
   cuda_check(cub::DeviceScan::InclusiveSum(nullptr, tmp, static_cast<const float*>(nullptr), static_cast<float*>(nullptr),
-                                           static_cast<int>(items > 0 ? items : 1)),
+                                           static_cast<long long>(items > 0 ? items : 1)),
              "scan size");
   const size_t nb = near_sym_tiles(n);
   return 4 * nb * sizeof(double) + 2 * static_cast<size_t>(items) * sizeof(float) + tmp + 65 * sizeof(long) + 6 * 256;
 }
 
 void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_host, void* ws, size_t ws_bytes,
-                    int* row_start_dev, int* row_start_host, cudaStream_t st) {
+                    long long* row_start_dev, long long* row_start_host, cudaStream_t st) {
   int tile = 0, chunk = 0;
   near_sym_shape(kind, &tile, &chunk);
   const int nb = static_cast<int>((a.nt + tile - 1) / tile);
   long items = 0;
   for (int I = 0; I < nb; ++I) {
-    row_start_host[I] = static_cast<int>(items);
+    row_start_host[I] = items;
     items += (nb - I + chunk - 1) / chunk;
   }
-  row_start_host[nb] = static_cast<int>(items);
+  row_start_host[nb] = items;
   auto align = [](size_t v) { return (v + 255) & ~static_cast<size_t>(255); };
   char* base = static_cast<char*>(ws);
   double* box = reinterpret_cast<double*>(base);
@@ -195,13 +245,13 @@ void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_ho
   off += align(65 * sizeof(long));
   if (off > ws_bytes || world > 64) throw_internal("near_sym_split: workspace");
   size_t tmp = ws_bytes - off;
-  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(long long), cudaMemcpyHostToDevice, st),
              "row starts");
   tile_box_kernel<<<static_cast<unsigned>((static_cast<size_t>(nb) * 32 + 255) / 256), 256, 0, st>>>(a.tgt, a.nt, tile,
                                                                                                     nb, box);
   item_cost_kernel<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(box, row_start_dev, nb, chunk, items,
                                                                                 a, cost);
-  cuda_check(cub::DeviceScan::InclusiveSum(base + off, tmp, cost, prefix, static_cast<int>(items), st), "scan");
+  cuda_check(cub::DeviceScan::InclusiveSum(base + off, tmp, cost, prefix, static_cast<long long>(items), st), "scan");
   split_kernel<<<1, 128, 0, st>>>(prefix, items, world, bounds);
   count_launches(3);
   cuda_check(cudaMemcpyAsync(bounds_host, bounds, (world + 1) * sizeof(long), cudaMemcpyDeviceToHost, st), "D2H bounds");
@@ -224,8 +274,8 @@ bool near_sym_supported(NearKind kind) {
          kind == NearKind::Stokes || kind == NearKind::StokesP;
 }
 
-bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
-                     const SymRange& r) {
+bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd,
+                     long long* rsh, const SymRange& r) {
   if (a.nt == 0) {
     if (r.total_items) *r.total_items = 0;
     return true;

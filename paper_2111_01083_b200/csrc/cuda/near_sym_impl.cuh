@@ -105,7 +105,22 @@ constexpr int kWarps = kT / 32;
 // sign of v and each remainder is exact. Layout: target-major, the three limbs of
 // output c of target l at acc[(l * nout + c) * 3 + {0,1,2}], so a contiguous slice of
 // targets is a contiguous slice of the buffer (the multi-GPU reduce-scatter operand).
-__device__ __forceinline__ void fx_add(unsigned long long* p, double v) {
+//
+// Values are scaled by an exact power of two 2^k before the split (and by 2^-k in the
+// readout), k = fx_exponent(max |strength|, n): the scaled sum over all n sources of
+// |strength| stays below 2^24, so the accumulator's resolution and range follow the
+// strengths the way fp64 summation does (the reference sums in plain fp64,
+// apply.cpp:532-540) -- strengths of 1e-15 or 1e15 give the same relative accuracy as
+// O(1) ones. A scaled value at or beyond 2^84 (limb a would overflow), inf or NaN raises
+// flag bit 1 (value 2) and the engine redoes the near field on the one-sided fp64 tile
+// (engine.cu Plan::near). The scale is re-read at each flush (one cached load per
+// thread and column tile) rather than held in a register across the tile loop.
+__device__ __forceinline__ void fx_add(unsigned long long* p, double v, const NearArgs& na) {
+  v *= fx_scale(fx_exponent(*na.fx_maxhi, na.ns));
+  if (!(fabs(v) < 0x1p84)) {
+    atomicOr(na.flag, 2);
+    return;
+  }
   const double a = trunc(v * 0x1p-22);
   const double r1 = fma(-a, 0x1p22, v);
   const double b = trunc(r1 * 0x1p20);
@@ -416,10 +431,10 @@ struct SymArgs {
   NearArgs a;
   int nb;                  // number of row tiles (kT * TPT points)
   int ncb;                 // number of column tiles (kT * CPT points)
-  int chunk;               // column tiles per work item
-  const int* row_start;    // [nb + 1] first work item of each row tile
-  unsigned long long* fx;  // fixed-point accumulators [n][nout][3]
-  int item0;               // first work item of this launch (multi-GPU item ranges)
+  int chunk;                   // column tiles per work item
+  const long long* row_start;  // [nb + 1] first work item of each row tile (int64: items grow as n^2)
+  unsigned long long* fx;      // fixed-point accumulators [n][nout][3]
+  long long item0;             // first work item of this launch (multi-GPU item ranges, 2^31-block chunks)
 };
 
 template <class K>
@@ -471,7 +486,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   __shared__ double s_keep[PWB_SYM_KEEP_SMEM && K::FAST ? TPT * K::NACC : 1][PWB_SYM_KEEP_SMEM && K::FAST ? kT : 1];
 
   // work item -> (row tile I, first column tile)
-  const int item = S.item0 + static_cast<int>(blockIdx.x);
+  const long long item = S.item0 + static_cast<long long>(blockIdx.x);
   int lo = 0, hi = S.nb;  // row_start[I] <= item < row_start[I+1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -481,7 +496,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       hi = mid;
   }
   const int I = lo;
-  const int J0 = I * R + (item - S.row_start[I]) * S.chunk;
+  const int J0 = I * R + static_cast<int>(item - S.row_start[I]) * S.chunk;
   const int J1 = min(S.ncb, J0 + S.chunk);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -736,10 +751,9 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       double o[K::NOUT];
       K::finish(acc, a, o);
 #pragma unroll
-      for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (j * K::NOUT + c) * 3, o[c]);
+      for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (j * K::NOUT + c) * 3, o[c], a);
     }
   }
-  if (flag) atomicOr(a.flag, 1);
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     if (!live[k]) continue;
@@ -747,8 +761,9 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     double o[K::NOUT];
     K::finish(racc[k], a, o);
 #pragma unroll
-    for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (l * K::NOUT + c) * 3, o[c]);
+    for (int c = 0; c < K::NOUT; ++c) fx_add(S.fx + (l * K::NOUT + c) * 3, o[c], a);
   }
+  if (flag) atomicOr(a.flag, 1);
 }
 
 
@@ -767,23 +782,23 @@ __global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ Sy
 }
 
 template <class K, int NXI, int NROW, bool USK = false>
-void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                      int* row_start_host, const SymRange& range) {
+void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* row_start_dev,
+                      long long* row_start_host, const SymRange& range) {
   constexpr int TILE = kT * K::TPT, CT = kT * K::CPT, R = TILE / CT;
   const int chunk = K::CHUNK;
   const int nb = static_cast<int>((a.nt + TILE - 1) / TILE);
   const int ncb = static_cast<int>((a.nt + CT - 1) / CT);
-  int items = 0;
+  long long items = 0;
   for (int I = 0; I < nb; ++I) {
     row_start_host[I] = items;
-    items += (ncb - I * R + chunk - 1) / chunk;
+    items += (ncb - static_cast<long long>(I) * R + chunk - 1) / chunk;
   }
   row_start_host[nb] = items;
   if (range.total_items) *range.total_items = items;
   if (range.count_only) return;
-  const long b = range.begin < 0 ? 0 : std::min<long>(range.begin, items);
-  const long e = range.end < 0 ? items : std::min<long>(range.end, items);
-  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+  const long long b = range.begin < 0 ? 0 : std::min<long long>(range.begin, items);
+  const long long e = range.end < 0 ? items : std::min<long long>(range.end, items);
+  cuda_check(cudaMemcpyAsync(row_start_dev, row_start_host, (nb + 1) * sizeof(long long), cudaMemcpyHostToDevice, st),
              "row starts");
   const size_t nout = K::NOUT;
   if (range.finish) cuda_check(cudaMemsetAsync(fx, 0, 3 * a.nt * nout * sizeof(unsigned long long), st), "memset fx");
@@ -794,31 +809,24 @@ void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx
   S.chunk = chunk;
   S.row_start = row_start_dev;
   S.fx = fx;
-  S.item0 = static_cast<int>(b);
-  if (e > b) {
-    // Static shared memory (tile + per-warp column partials) is what limits residency
-    // next to registers: ask for the maximum carveout so registers decide (ncu r1: the
-    // default carveout capped SymLaplace at 5 blocks on shared memory alone).
-    static bool carveout = false;
-    void (*kern)(const SymArgs);
-    if constexpr (K::MINB > 0)
-      kern = near_sym_kernel_capped<K, NXI, NROW, USK>;
-    else
-      kern = near_sym_kernel<K, NXI, NROW, USK>;
-    if (!carveout) {
-      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      cudaSharedmemCarveoutMaxShared),
-                 "smem carveout");
-      carveout = true;
-    }
-    kern<<<static_cast<unsigned>(e - b), kT, 0, st>>>(S);
+  void (*kern)(const SymArgs);
+  if constexpr (K::MINB > 0)
+    kern = near_sym_kernel_capped<K, NXI, NROW, USK>;
+  else
+    kern = near_sym_kernel<K, NXI, NROW, USK>;
+  if (e > b) set_max_carveout(reinterpret_cast<const void*>(kern));
+  // grids of at most 2^31 - 1 blocks (items grow as n^2: ~2^31 near n ~ 1e8 for Laplace)
+  constexpr long long kMaxGrid = 0x7fffffffLL;
+  for (long long i0 = b; i0 < e; i0 += kMaxGrid) {
+    S.item0 = i0;
+    kern<<<static_cast<unsigned>(std::min(kMaxGrid, e - i0)), kT, 0, st>>>(S);
     count_launches(1);
   }
-  if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, a.out_row, st);
+  if (range.finish) launch_fx_finish(fx, a.nt, a.out0, a.nout0, a.out1, a.nout1, a.out_row, a.fx_maxhi, a.ns, 0, a.flag, st);
 }
 
 template <class K>
-bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
+bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd, long long* rsh,
                   const SymRange& r) {
   if (a.nxi == 3 && a.nrow == 1) return launch_sym_shape<K, 3, 1>(a, st, fx, rsd, rsh, r), true;
   // unskewed 3x3 (c1, c3, c5's cells): the fast tiles form each column's rx once per pair
@@ -830,12 +838,12 @@ bool dispatch_sym(const NearArgs& a, cudaStream_t st, unsigned long long* fx, in
 }
 
 // per-family entry points (one translation unit each)
-bool launch_laplace(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
+bool launch_laplace(const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd, long long* rsh,
                     const SymRange& r);
-bool launch_modhelm(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd,
-                    int* rsh, const SymRange& r);
-bool launch_stokes(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd,
-                   int* rsh, const SymRange& r);
+bool launch_modhelm(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd,
+                    long long* rsh, const SymRange& r);
+bool launch_stokes(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd,
+                   long long* rsh, const SymRange& r);
 
 }  // namespace sym
 }  // namespace pwb

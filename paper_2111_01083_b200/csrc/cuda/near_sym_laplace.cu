@@ -4,7 +4,7 @@
 namespace pwb {
 namespace sym {
 
-bool launch_laplace(const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd, int* rsh,
+bool launch_laplace(const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd, long long* rsh,
                     const SymRange& r) {
   if (a.lowp && a.coarse_log) return dispatch_sym<SymLaplace<true, true>>(a, st, fx, rsd, rsh, r);
   return a.lowp ? dispatch_sym<SymLaplace<true>>(a, st, fx, rsd, rsh, r)

@@ -4,8 +4,8 @@
 namespace pwb {
 namespace sym {
 
-bool launch_modhelm(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd,
-                    int* rsh, const SymRange& r) {
+bool launch_modhelm(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd,
+                    long long* rsh, const SymRange& r) {
   // a.lowp: 0 full tier, 1 reduced (eps >= 1e-11), 2 coarse Bessel (eps >= 1e-9)
   if (kind == NearKind::ModHelmGrad)
     return a.lowp == 2 ? dispatch_sym<SymModHelm<true, true, true>>(a, st, fx, rsd, rsh, r)

@@ -4,8 +4,8 @@
 namespace pwb {
 namespace sym {
 
-bool launch_stokes(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* rsd,
-                   int* rsh, const SymRange& r) {
+bool launch_stokes(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* rsd,
+                   long long* rsh, const SymRange& r) {
   if (kind == NearKind::StokesP)
     return a.lowp ? dispatch_sym<SymStokes<true, true>>(a, st, fx, rsd, rsh, r)
                   : dispatch_sym<SymStokes<true, false>>(a, st, fx, rsd, rsh, r);

@@ -450,25 +450,23 @@ void launch_exact_lines(const double* g, int lines, int nf, const double* s, int
   count_launches(1);
 }
 
-// batched in-place complex transform of `lines` lines of nf points; sign +1 = e^{+i}
-void fft_lines(double* data, int nf, int lines, int sign, cudaStream_t st) {
-  static std::mutex mu;
-  static std::map<std::pair<int, int>, cufftHandle> plans;
-  cufftHandle plan;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_pair(nf, lines);
-    auto it = plans.find(key);
-    if (it == plans.end()) {
-      int n[1] = {nf};
-      fft_check(cufftPlanMany(&plan, 1, n, nullptr, 1, nf, nullptr, 1, nf, CUFFT_Z2Z, lines), "cufftPlanMany");
-      it = plans.emplace(key, plan).first;
-    }
-    plan = it->second;
-    fft_check(cufftSetStream(plan, st), "cufftSetStream");
-    auto* z = reinterpret_cast<cufftDoubleComplex*>(data);
-    fft_check(cufftExecZ2Z(plan, z, z, sign > 0 ? CUFFT_INVERSE : CUFFT_FORWARD), "cufftExecZ2Z");
+FftPlans::~FftPlans() {
+  for (auto& kv : plans_) cufftDestroy(static_cast<cufftHandle>(kv.second));
+}
+
+void FftPlans::exec(double* data, int nf, int lines, int sign, cudaStream_t st) {
+  auto key = std::make_pair(nf, lines);
+  auto it = plans_.find(key);
+  if (it == plans_.end()) {
+    cufftHandle plan;
+    int n[1] = {nf};
+    fft_check(cufftPlanMany(&plan, 1, n, nullptr, 1, nf, nullptr, 1, nf, CUFFT_Z2Z, lines), "cufftPlanMany");
+    it = plans_.emplace(key, static_cast<int>(plan)).first;
   }
+  const cufftHandle plan = static_cast<cufftHandle>(it->second);
+  fft_check(cufftSetStream(plan, st), "cufftSetStream");
+  auto* z = reinterpret_cast<cufftDoubleComplex*>(data);
+  fft_check(cufftExecZ2Z(plan, z, z, sign > 0 ? CUFFT_INVERSE : CUFFT_FORWARD), "cufftExecZ2Z");
   count_launches(1);
 }
 
@@ -527,8 +525,9 @@ void fast_type1_dev(double eps, size_t n, const double* x, const double* c, size
   a.beta = s.beta;
   a.lines = 1;
   DevBuf ws;
+  FftPlans fft;  // destroyed after the final synchronize below
   launch_spread(a, static_cast<double*>(g.p), ws, device_sms(), st);
-  fft_lines(static_cast<double*>(g.p), static_cast<int>(nf), 1, +1, st);
+  fft.exec(static_cast<double*>(g.p), static_cast<int>(nf), 1, +1, st);
   launch_deconv(static_cast<double*>(g.p), 1, static_cast<int>(nf), static_cast<int>(nmodes), fac_d, f, st);
   cuda_check(cudaStreamSynchronize(st), "sync");
 }
@@ -543,8 +542,9 @@ void fast_type2_dev(double eps, size_t n, const double* x, size_t nmodes, const 
   Scoped g, fac;
   cuda_check(cudaMalloc(&g.p, 2 * nf * sizeof(double)), "cudaMalloc");
   double* fac_d = upload_vec(fac, deconv_factors(s, nf, nmodes), st);
+  FftPlans fft;  // destroyed after the final synchronize below
   launch_precorrect(f, 1, static_cast<int>(nf), static_cast<int>(nmodes), fac_d, static_cast<double*>(g.p), st);
-  fft_lines(static_cast<double*>(g.p), static_cast<int>(nf), 1, -1, st);
+  fft.exec(static_cast<double*>(g.p), static_cast<int>(nf), 1, -1, st);
   SpreadArgs a;
   a.n = n;
   a.pos = PosKind::Array;

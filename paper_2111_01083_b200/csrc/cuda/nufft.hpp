@@ -58,6 +58,5 @@ void launch_precorrect(const double* f, int lines, int nf, int nmodes, const dou
 void launch_mix(const MixArgs& a, const double* F, double* G, cudaStream_t st);
 void launch_exact_lines(const double* g, int lines, int nf, const double* s, int ns, double hx, const double* fac3,
                         double* f, cudaStream_t st);
-void fft_lines(double* data, int nf, int lines, int sign, cudaStream_t st);
 
 }  // namespace pwb

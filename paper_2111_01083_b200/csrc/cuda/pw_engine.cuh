@@ -6,6 +6,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -25,6 +26,35 @@ void cuda_check(cudaError_t e, const char* what);
 // Number of kernels this process has launched through the engine (pwb_launch_count).
 void count_launches(long n);
 long launch_count();
+// Max shared-memory carveout for a kernel, once per (device, kernel).
+void set_max_carveout(const void* kernel);
+
+// ---------------------------------------------------------------- fixed-point scale
+// Exponent k of the symmetric tile's fixed-point scale 2^k (near_sym_impl.cuh fx_add):
+// maxhi = high word of max |strength| (its bit order is the order of the non-negative
+// doubles), n = number of sources; 2^e > max |strength| and 2^lg >= n, so the scaled
+// sum of |strength| over all sources is below 2^24. Non-finite or all-zero strengths: 0.
+__host__ __device__ inline int fx_exponent(unsigned maxhi, size_t n) {
+  if (maxhi == 0u || maxhi >= 0x7ff00000u) return 0;
+  const int e = static_cast<int>(maxhi >> 20) - 1023 + 1;
+#ifdef __CUDA_ARCH__
+  const int lg = n > 1 ? 64 - __clzll(static_cast<long long>(n - 1)) : 0;
+#else
+  const int lg = n > 1 ? 64 - __builtin_clzll(static_cast<unsigned long long>(n - 1)) : 0;
+#endif
+  const int k = 24 - e - lg;
+  return k < -960 ? -960 : (k > 960 ? 960 : k);
+}
+__host__ __device__ inline double fx_scale(int k) {  // 2^k, |k| <= 960
+  const long long bits = static_cast<long long>(1023 + k) << 52;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(bits);
+#else
+  double v;
+  std::memcpy(&v, &bits, sizeof v);
+  return v;
+#endif
+}
 
 // ---------------------------------------------------------------- near field
 enum class NearKind { Laplace, ModHelm, ModHelmGrad, Stokes, StokesP, ModStokes, ModStokesP, Stresslet, Multipole };
@@ -49,7 +79,8 @@ struct NearArgs {
   double* partial = nullptr;
   int splits = 1;
   size_t src_per_split = 0;
-  int* flag = nullptr;     // set to 1 on a non-identity exact coincidence
+  int* flag = nullptr;     // bit 0: a non-identity exact coincidence; bit 1: fixed-point range exceeded
+  const unsigned* fx_maxhi = nullptr;  // symmetric tiles: high word of max |strength| (launch_fx_maxhi)
   const int* out_row = nullptr;  // binned targets: output row of target l (nullptr: l)
   int lowp = 0;                  // near tiles: reduced-precision tier (eps >= 1e-11, pw_math.cuh)
   int cull = 1;                  // screened symmetric tiles: per-tile image mask (near_sym_impl.cuh)
@@ -74,7 +105,7 @@ void scatter_add_rows(const unsigned long long* in, const int* perm, size_t n, i
 size_t near_outputs(NearKind kind);
 void launch_near(NearKind kind, const NearArgs& a, cudaStream_t st, double* partial_ws, int sm_count);
 // Symmetric (targets == sources) fused near images: each unordered pair once
-// (near_sym.cu). fx: 3 * n * nout uint64 accumulators; row_start: nb + 1 ints
+// (near_sym.cu). fx: 3 * n * nout uint64 accumulators; row_start: nb + 1 int64
 // (device and pinned host). Returns false when the kind/layout has no symmetric form.
 bool near_sym_supported(NearKind kind);
 size_t near_sym_tiles(size_t n);
@@ -88,10 +119,14 @@ struct SymRange {
   bool count_only = false;
   long* total_items = nullptr;
 };
-bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx, int* row_start_dev,
-                     int* row_start_host, const SymRange& range);
+bool launch_near_sym(NearKind kind, const NearArgs& a, cudaStream_t st, unsigned long long* fx,
+                     long long* row_start_dev, long long* row_start_host, const SymRange& range);
+// *maxhi = high word of max over the sources of |q| / |f.x|, |f.y| (zeroed first).
+void launch_fx_maxhi(const NearArgs& a, unsigned* maxhi, cudaStream_t st);
+// out += fixed-point accumulators * 2^-k, k = fx_exponent(*maxhi_dev, n_src) when maxhi_dev
+// is given, else k_host; skipped entirely when flag bit 1 (overflow) is set.
 void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int nout0, double* out1, int nout1,
-                      const int* out_row,
+                      const int* out_row, const unsigned* maxhi_dev, size_t n_src, int k_host, const int* flag,
                       cudaStream_t st);
 // host-only: number of work items of the symmetric decomposition (0 if none)
 long near_sym_item_count(NearKind kind, size_t n);
@@ -101,7 +136,7 @@ void near_sym_shape(NearKind kind, int* tile, int* chunk);
 // tile boxes of the (binned) points in a.tgt, estimated item costs, prefix sum, split.
 size_t near_sym_split_bytes(size_t n, long items);
 void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_host, void* ws, size_t ws_bytes,
-                    int* row_start_dev, int* row_start_host, cudaStream_t st);
+                    long long* row_start_dev, long long* row_start_host, cudaStream_t st);
 
 // ---------------------------------------------------------------- far field (direct S2PW / PW2T)
 // Weight sets: what each source contributes per mode (K real weights).

@@ -9,6 +9,8 @@ The path shards with exactly two exchange steps:
   work items (pwb_near_sym_items); every rank runs a contiguous item range into its
   own int64 fixed-point accumulator over ALL targets, one reduce-scatter (int64 sum,
   exact and order-independent) hands each rank the accumulator of its target slice.
+  Before it, one tiny all-reduce (MAX) of the ranks' status words: a coincidence any
+  rank found raises the reference's CoincidentSourceTarget on every rank.
   With separate targets the near field is target-sharded with no exchange.
 
 Outputs stay sharded: rank r owns targets [r*chunk, min(n, (r+1)*chunk)),
@@ -47,6 +49,13 @@ class Comm:
             import torch.distributed as dist
 
             dist.all_reduce(t)
+        return t
+
+    def allreduce_max(self, t):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t
 
     def reduce_scatter(self, inp, out):
@@ -105,10 +114,22 @@ def sharded_total_field(backend, comm: Comm, plan: ShardPlan, symmetric: bool):
         else:
             i_lo, i_hi = contiguous(items, plan.world, plan.rank)
         acc = backend.accumulator(plan.chunk * plan.world * nout * 3)
-        backend.near_partial(i_lo, i_hi, acc)
+        scale_exp, status = backend.near_partial(i_lo, i_hi, acc)
+        # agree on the status before the reduce-scatter: a coincidence seen by one rank
+        # raises CoincidentSourceTarget on every rank (no peer left blocked in the
+        # collective); the fixed-point scale must be the same everywhere (it is derived
+        # from the global strengths) -- max(k) == -max(-k) checks it
+        flags = comm.allreduce_max(backend.small_ints([status, scale_exp, -scale_exp]))
+        status, k_hi, k_lo = (int(v) for v in flags.tolist())
+        from . import raise_sym_status
+
+        raise_sym_status(status)
+        if k_hi != -k_lo:
+            raise RuntimeError(f"ranks disagree on the fixed-point scale ({-k_lo}..{k_hi}): "
+                               "every rank must hold the same strengths")
         mine = backend.accumulator(plan.chunk * nout * 3)
         comm.reduce_scatter(acc, mine)
-        backend.fixed_to_out(mine, t_hi - t_lo, out)
+        backend.fixed_to_out(mine, t_hi - t_lo, out, scale_exp)
     else:
         backend.near_targets(t_lo, t_hi, out)
     return out, (t_lo, t_hi)
@@ -145,17 +166,21 @@ class CudaBackend:
     def accumulator(self, n):
         return self.torch.zeros(n, dtype=self.torch.int64, device=self.dev)
 
+    def small_ints(self, vals):
+        return self.torch.tensor(vals, dtype=self.torch.int64, device=self.dev)
+
     def near_partial(self, lo, hi, acc):
+        """-> (scale_exp, status) of pwb_near_sym_partial."""
         sys_ = self.pw.ParticleSystem(sources=self.src, targets=self.src, **{self.kw: self.q})
-        self.pw.near_sym_partial(self.pz, sys_, acc, lo, hi, self.opt)
+        return self.pw.near_sym_partial(self.pz, sys_, acc, lo, hi, self.opt)
 
     def near_split(self, world):
         sys_ = self.pw.ParticleSystem(sources=self.src, targets=self.src, **{self.kw: self.q})
         return self.pw.near_sym_split(self.pz, sys_, world, self.opt)
 
-    def fixed_to_out(self, acc, n, out):
+    def fixed_to_out(self, acc, n, out, scale_exp):
         ref = out.scalar if out.scalar is not None else out.velocity
-        self.pw.fixed_to_field(self.pz, acc, n, out, self.opt, like=ref)
+        self.pw.fixed_to_field(self.pz, acc, n, out, self.opt, like=ref, scale_exp=scale_exp)
 
     def near_targets(self, lo, hi, out):
         sys_ = self.pw.ParticleSystem(sources=self.src, targets=self.tgt[lo:hi], **{self.kw: self.q})

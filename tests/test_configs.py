@@ -51,3 +51,22 @@ def test_full_sizes_match_baseline(pw):
     assert [configs.CONFIGS[k].n_src for k in ("c1", "c2", "c3", "c4", "c5")] == [1000, 100000, 1000000, 1000000,
                                                                                  10000000]
     assert [configs.CONFIGS[k].eps for k in ("c1", "c2", "c3", "c4", "c5")] == [1e-10, 1e-10, 1e-8, 1e-10, 1e-8]
+
+
+def test_reference_arm_draws_the_same_bytes(pw):
+    """bench.py's reference arm draws its inputs from the reference's own Rng in oracle/_ref
+    (or the C restatement), never from the product library: same bytes for every config."""
+    import workloads
+    from oracle import pyoracle
+    from paper_2111_01083_b200 import configs
+
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        a = configs.generate(name, n_src=3000)
+        b = workloads.generate(name, n_src=3000, rng=pyoracle.rng_uniform)
+        assert np.array_equal(a.sources, b.sources) and np.array_equal(a.targets, b.targets)
+        assert np.array_equal(a.sample, b.sample)
+        sa = a.charges if a.charges is not None else a.forces
+        sb = b.charges if b.charges is not None else b.forces
+        assert np.array_equal(sa, sb)
+    if pyoracle.ref_available():
+        assert np.array_equal(pyoracle.Ref().rng_uniform(77, 5000), pyoracle.Port().rng_uniform(77, 5000))

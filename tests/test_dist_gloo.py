@@ -15,6 +15,15 @@ from conftest import ROOT
 TILE, CHUNK = 4, 2
 
 
+def _fx_exponent(maxabs, n):
+    """Mirror of pw_engine.cuh fx_exponent: 2^e > max|q|, 2^lg >= n, k = 24 - e - lg."""
+    if maxabs == 0.0 or not np.isfinite(maxabs):
+        return 0
+    e = int(np.frexp(maxabs)[1])  # maxabs < 2^e (frexp mantissa in [0.5, 1))
+    lg = int(n - 1).bit_length() if n > 1 else 0
+    return int(np.clip(24 - e - lg, -960, 960))
+
+
 def _fx_split(v):
     a = np.trunc(v * 2.0 ** -22)
     r1 = v - a * 2.0 ** 22
@@ -97,13 +106,21 @@ class NumpyBackend:
         g = 0.0
         for k, (sx, sy) in enumerate(self.shifts):
             rx, ry = (t[0] - s[0]) - sx, (t[1] - s[1]) - sy
-            if rx == 0.0 and ry == 0.0:
-                assert identity_skip and k == self.ident
+            if rx == 0.0 and ry == 0.0:  # apply.cpp:538-545: skip in the identity image, else flag
+                if not (identity_skip and k == self.ident):
+                    self.status |= 1
                 continue
             g += -np.log(rx * rx + ry * ry) / (4 * np.pi)
         return g
 
+    def small_ints(self, vals):
+        return self.torch.tensor(vals, dtype=self.torch.int64)
+
     def near_partial(self, lo, hi, acc):
+        """Same contract as pwb_near_sym_partial: (scale_exp, status), no raise."""
+        self.status = 0
+        k = _fx_exponent(float(np.max(np.abs(self.q))), self.n)
+        sc = 2.0 ** k
         a = acc.numpy().reshape(-1, 1, 3)
         for I, J0, J1 in self._items()[lo:hi]:
             rows = range(I * TILE, min(self.n, (I + 1) * TILE))
@@ -121,30 +138,33 @@ class NumpyBackend:
                             cacc[j] += self.q[l] * g
                 if J != I:
                     for j, v in cacc.items():
-                        a[j, 0] += _fx_split(np.float64(v))
+                        a[j, 0] += _fx_split(np.float64(v) * sc)
             for l, v in racc.items():
-                a[l, 0] += _fx_split(np.float64(v))
+                a[l, 0] += _fx_split(np.float64(v) * sc)
+        return k, self.status
 
-    def fixed_to_out(self, acc, n, out):
-        v = _fx_value(acc.numpy().reshape(-1, 3)[:n])
+    def fixed_to_out(self, acc, n, out, scale_exp):
+        v = _fx_value(acc.numpy().reshape(-1, 3)[:n]) * 2.0 ** -scale_exp
         out.scalar += self.torch.from_numpy(v)
 
     def near_targets(self, lo, hi, out):
         raise AssertionError("symmetric path expected")
 
 
-def _system(pw):
+def _system(pw, coincident=False, scale=1.0):
     rng = np.random.default_rng(5)
     n = 37  # not a multiple of the world size or the tile
     src = np.ascontiguousarray(np.stack([rng.uniform(-0.5, 0.5, n), rng.uniform(-0.5, 0.5, n)], 1))
-    q = rng.uniform(-1, 1, n)
+    if coincident:  # the last point is the first one's image under the shift (d, 0): the pair
+        src[0, 0], src[-1] = -0.5, (0.5, src[0, 1])  # lies in the last row tile, one rank's items only
+    q = rng.uniform(-1, 1, n) * scale
     q -= q.mean()
     cell = pw.make_unit_cell(1.0, 0.0, 1.0)
     pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-6)
     return pz, src, q
 
 
-def _worker(rank, world, port, outdir, uneven=False):
+def _worker(rank, world, port, outdir, uneven=False, coincident=False, scale=1.0):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -156,13 +176,20 @@ def _worker(rank, world, port, outdir, uneven=False):
     import paper_2111_01083_b200 as pw
     from paper_2111_01083_b200 import dist as pdist
 
-    pz, src, q = _system(pw)
+    pz, src, q = _system(pw, coincident, scale)
     be = NumpyBackend(pw, pz, src, q)
     if uneven:  # a cost-balanced split (CudaBackend.near_split) need not be even: 80 / 20
         items = be.near_items()[0]
         be.near_split = lambda w: [0, (4 * items) // 5, items]
     plan = pdist.ShardPlan(len(src), len(src), world, rank)
-    out, (lo, hi) = pdist.sharded_total_field(be, pdist.Comm(world), plan, symmetric=True)
+    try:
+        out, (lo, hi) = pdist.sharded_total_field(be, pdist.Comm(world), plan, symmetric=True)
+    except pw.PeriwaveError as e:  # every rank must raise the same error (no hang)
+        with open(os.path.join(outdir, f"err{rank}.txt"), "w") as f:
+            f.write(e.code.name)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     np.save(os.path.join(outdir, f"r{rank}.npy"), np.concatenate([[lo, hi], out.scalar.numpy()]))
     dist.barrier()
     dist.destroy_process_group()
@@ -271,3 +298,40 @@ def test_two_ranks_gloo_uneven_item_split(pw, port, tmp_path):
         outs[uneven] = np.concatenate([np.load(d / f"r{r}.npy")[2:] for r in range(world)])
     a, b = outs[False], outs[True]
     assert np.max(np.abs((a - a.mean()) - (b - b.mean()))) <= 1e-13 * np.max(np.abs(a))
+
+
+def test_two_ranks_coincidence_raises_on_every_rank(pw, port, tmp_path):
+    """A coincident pair lives in one rank's item range only; the status all-reduce makes
+    every rank raise CoincidentSourceTarget (apply.cpp:544-545) instead of the owner
+    raising while its peer blocks in the reduce-scatter."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), False, True), nprocs=world, join=True,
+                       start_method="spawn")
+    assert [(tmp_path / f"err{r}.txt").read_text() for r in range(world)] == ["CoincidentSourceTarget"] * 2
+    # exactly one rank's item range holds the pair
+    pz, src, q = _system(pw, coincident=True)
+    be = NumpyBackend(pw, pz, src, q)
+    items, _ = be.near_items()
+    from paper_2111_01083_b200 import dist as pdist
+
+    seen = [be.near_partial(*pdist.contiguous(items, 2, r), be.accumulator(37 * 3))[1] for r in range(2)]
+    assert sorted(seen) == [0, 1]
+
+
+@pytest.mark.parametrize("scale", [1e-15, 1e15])
+def test_two_ranks_scaled_strengths(pw, port, tmp_path, scale):
+    """The fixed-point scale follows the strengths: results scale exactly with them."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    outs = {}
+    for sc in (1.0, scale):
+        d = tmp_path / f"s{sc:g}"
+        d.mkdir()
+        mp.start_processes(_worker, args=(world, _free_port(), str(d), False, False, sc), nprocs=world, join=True,
+                           start_method="spawn")
+        outs[sc] = np.concatenate([np.load(d / f"r{r}.npy")[2:] for r in range(world)])
+    a, b = outs[1.0], outs[scale] / scale
+    assert np.max(np.abs((a - a.mean()) - (b - b.mean()))) <= 1e-12 * np.max(np.abs(a))

@@ -45,7 +45,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        pw.near_sym_partial(pz, s, acc, lo, hi, opt)
+        pw.near_sym_partial(pz, s, acc, lo, hi, opt)  # -> (scale_exp, status)
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
