@@ -70,3 +70,16 @@ def test_reference_arm_draws_the_same_bytes(pw):
         assert np.array_equal(sa, sb)
     if pyoracle.ref_available():
         assert np.array_equal(pyoracle.Ref().rng_uniform(77, 5000), pyoracle.Port().rng_uniform(77, 5000))
+
+
+def test_workload_ordinals_match_the_api(pw):
+    """workloads.py restates periwave::Pde / Periodicity as plain ints (cell.hpp:9,
+    kernels.hpp:7): they must be the product enums' values, or every config changes cell."""
+    import workloads
+
+    assert (workloads.POISSON, workloads.MODHELMHOLTZ, workloads.STOKES) == (
+        pw.Pde.Poisson, pw.Pde.ModHelmholtz, pw.Pde.Stokes)
+    assert (workloads.SINGLY, workloads.DOUBLY) == (pw.Periodicity.Singly, pw.Periodicity.Doubly)
+    per = {k: pw.Periodicity(c.cell[3]) for k, c in workloads.CONFIGS.items()}
+    assert per == {"c1": pw.Periodicity.Doubly, "c2": pw.Periodicity.Doubly, "c3": pw.Periodicity.Doubly,
+                   "c4": pw.Periodicity.Singly, "c5": pw.Periodicity.Doubly}

@@ -31,7 +31,7 @@ import numpy as np
 # ordinals of periwave::Pde / Periodicity (proj/include/periwave/cell.hpp); the product's
 # IntEnums compare and hash equal to these ints
 POISSON, MODHELMHOLTZ, STOKES = 0, 1, 2
-SINGLY, DOUBLY = 0, 1
+SINGLY, DOUBLY = 1, 2
 
 
 @dataclass(frozen=True)
