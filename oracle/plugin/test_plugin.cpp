@@ -1,0 +1,177 @@
+// TEST INFRASTRUCTURE: the reference's own total_field with the B200 near field plugged in
+// (include/periwave_b200_plugin.hpp), against the reference's stock FreeSpaceEvaluator.
+//
+// Compiled against the reference headers (proj/include) and linked to the UNMODIFIED
+// reference library (oracle/_ref/libperiwave_ref.so, first in link order so every
+// periwave:: call of this program binds to the reference) and to libperiwave_b200.so
+// (C-ABI only). Built by oracle/Makefile `plugin`; run by tests/test_gpu_plugin.py.
+//
+// Pattern: the reference's "near-field evaluator override is honored" test
+// (proj/tests/test_apply.cpp:337-357): the override is called once per near image and the
+// result matches the stock evaluator -- here within 1e-13 relative (the GPU sums in a
+// different order / with its own K0), not bitwise.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "periwave/apply.hpp"
+#include "periwave/periodize.hpp"
+#include "periwave/util.hpp"
+#include "periwave_b200_plugin.hpp"
+
+using namespace periwave;
+
+namespace {
+
+int failures = 0;
+
+void report(const std::string& name, bool ok, const std::string& detail) {
+  std::printf("{\"case\": \"%s\", \"ok\": %s, %s}\n", name.c_str(), ok ? "true" : "false", detail.c_str());
+  if (!ok) ++failures;
+}
+
+std::vector<Vec2> points(const UnitCell& c, Rng& rng, std::size_t n) {
+  std::vector<Vec2> p(n);
+  for (auto& v : p) {
+    const double x1 = rng.uniform() - 0.5, x2 = rng.uniform() - 0.5;
+    v = {x1 * c.d + x2 * c.xi, x2 * c.eta};
+  }
+  return p;
+}
+
+double rel(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+std::vector<double> flat(const FieldResult& r) {
+  std::vector<double> v(r.scalar);
+  for (const auto& u : r.velocity) {
+    v.push_back(u.x);
+    v.push_back(u.y);
+  }
+  v.insert(v.end(), r.pressure.begin(), r.pressure.end());
+  for (const auto& z : r.complex_scalar) {
+    v.push_back(z.real());
+    v.push_back(z.imag());
+  }
+  return v;
+}
+
+std::string num(const char* k, double v) {
+  char b[96];
+  std::snprintf(b, sizeof b, "\"%s\": %.3e", k, v);
+  return b;
+}
+
+// total_field with the plug-in vs the stock evaluator: agreement, one call per image
+void compare(const std::string& name, const Periodizer& pz, const ParticleSystem& sys, const ApplyOptions& opt,
+             double tol) {
+  periwave_b200::NearEvaluator gpu;
+  const FieldResult a = total_field(pz, sys, opt, &gpu);
+  const FieldResult b = total_field(pz, sys, opt);
+  const int images = static_cast<int>(near_translations(pz.cell).size());
+  const double e = rel(flat(a), flat(b));
+  report(name, e <= tol && gpu.calls() == images && a.accelerated == b.accelerated,
+         num("rel_l2", e) + ", \"calls\": " + std::to_string(gpu.calls()) + ", \"images\": " + std::to_string(images));
+}
+
+template <class F>
+void expect_error(const std::string& name, ErrorCode want, F&& f) {
+  try {
+    f();
+    report(name, false, "\"error\": \"none raised\"");
+  } catch (const Error& e) {
+    report(name, e.code() == want, "\"code\": " + std::to_string(static_cast<int>(e.code())));
+  } catch (const std::exception& e) {
+    report(name, false, std::string("\"error\": \"") + e.what() + "\"");
+  }
+}
+
+}  // namespace
+
+int run() {
+  Rng rng(2111);
+  {  // c1 shape: doubly periodic Poisson, square cell, targets = sources (identity image skips)
+    UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Doubly);
+    ParticleSystem sys;
+    sys.sources = points(cell, rng, 1000);
+    sys.charges.resize(1000);
+    double mean = 0.0;
+    for (double& q : sys.charges) mean += (q = rng.uniform() * 2.0 - 1.0);
+    for (double& q : sys.charges) q -= mean / 1000.0;
+    sys.targets = sys.sources;
+    compare("c1_poisson_self", make_periodizer(Pde::Poisson, 0.0, cell, 1e-10), sys, {}, 1e-13);
+  }
+  {  // c2 shape: modified Helmholtz beta = 10 on the skewed cell, separate targets (m0 = 2)
+    UnitCell cell = make_unit_cell(1.0, 0.3, 0.8, Periodicity::Doubly);
+    ParticleSystem sys;
+    sys.sources = points(cell, rng, 2000);
+    sys.targets = points(cell, rng, 1500);
+    sys.charges.resize(2000);
+    for (double& q : sys.charges) q = rng.uniform() * 2.0 - 1.0;
+    compare("c2_modhelm_skewed", make_periodizer(Pde::ModHelmholtz, 10.0, cell, 1e-10), sys, {}, 1e-13);
+  }
+  {  // Stokes with pressure, singly periodic
+    UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Singly);
+    ParticleSystem sys;
+    sys.sources = points(cell, rng, 700);
+    sys.targets = points(cell, rng, 500);
+    sys.forces.resize(700);
+    Vec2 mean{0.0, 0.0};
+    for (auto& f : sys.forces) mean += (f = {rng.uniform() - 0.5, rng.uniform() - 0.5});
+    for (auto& f : sys.forces) f = f - mean * (1.0 / 700.0);
+    ApplyOptions opt;
+    opt.with_pressure = true;
+    compare("stokes_pressure_singly", make_periodizer(Pde::Stokes, 0.0, cell, 1e-8), sys, opt, 1e-13);
+  }
+  {  // empty target list: sizes follow ensure_sizes, no device work
+    UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Doubly);
+    ParticleSystem sys;
+    sys.sources = points(cell, rng, 10);
+    sys.charges.assign(10, 0.0);
+    periwave_b200::NearEvaluator gpu;
+    FieldResult r;
+    gpu.accumulate(make_periodizer(Pde::ModHelmholtz, 1.0, cell, 1e-8), sys, {0.0, 0.0}, true, {}, r);
+    report("empty_targets", r.scalar.empty() && gpu.calls() == 1, "\"n\": 0");
+  }
+  {  // a target on a lattice image of a source: CoincidentSourceTarget like the stock one
+    UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Doubly);
+    ParticleSystem sys;
+    sys.sources = {{-0.5, 0.1}, {0.2, -0.3}};
+    sys.charges = {1.0, -1.0};
+    sys.targets = {{0.5, 0.1}};
+    const Periodizer pz = make_periodizer(Pde::Poisson, 0.0, cell, 1e-8);
+    periwave_b200::NearEvaluator gpu;
+    expect_error("coincident_plugin", ErrorCode::CoincidentSourceTarget, [&] { total_field(pz, sys, {}, &gpu); });
+    expect_error("coincident_stock", ErrorCode::CoincidentSourceTarget, [&] { total_field(pz, sys, {}); });
+  }
+  {  // strengths of the wrong length: the reference's LengthMismatch from the plug-in
+    UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Doubly);
+    ParticleSystem sys;
+    sys.sources = points(cell, rng, 5);
+    sys.charges = {1.0, 2.0};
+    sys.targets = points(cell, rng, 3);
+    periwave_b200::NearEvaluator gpu;
+    FieldResult r;
+    expect_error("length_mismatch", ErrorCode::LengthMismatch, [&] {
+      gpu.accumulate(make_periodizer(Pde::ModHelmholtz, 2.0, cell, 1e-8), sys, {0.0, 0.0}, true, {}, r);
+    });
+  }
+  std::printf("{\"failures\": %d}\n", failures);
+  return failures ? 1 : 0;
+}
+
+int main() {
+  try {
+    return run();
+  } catch (const std::exception& e) {
+    std::printf("{\"case\": \"uncaught\", \"ok\": false, \"error\": \"%s\"}\n", e.what());
+    return 1;
+  }
+}

@@ -4,7 +4,11 @@
 // signatures and error behaviour (periwave::Error thrown with the same codes).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "periwave/periwave.hpp"
@@ -35,10 +39,148 @@ K kind(const Periodizer& pz) {
   return K::Scalar;
 }
 
+// ---- one device plan per distinct periodizer
+// The reference passes the periodizer by const& to every call (apply.hpp:58-60); building a
+// device plan (stream, mode tables, NUFFT setup, workspaces) per call would cost more than a
+// small evaluation and all of a repeated one. The cache keys a wrapped periodizer by its
+// full content (every table byte), so equal periodizers share one plan and a modified copy
+// gets its own. A handful of recent entries are kept (LRU); the cache is intentionally never
+// destroyed (its plans hold CUDA resources that must not be freed during static teardown).
+class Bytes {
+ public:
+  template <class T>
+  void pod(const T& v) {
+    static_assert(std::is_trivially_copyable_v<T>);
+    const auto* p = reinterpret_cast<const unsigned char*>(&v);
+    b_.insert(b_.end(), p, p + sizeof(T));
+  }
+  template <class T>
+  void vec(const std::vector<T>& v) {
+    pod(v.size());
+    if (!v.empty()) {
+      const auto* p = reinterpret_cast<const unsigned char*>(v.data());
+      b_.insert(b_.end(), p, p + v.size() * sizeof(T));
+    }
+  }
+  void modes(const ModeSet& m) {
+    pod(m.axis);
+    vec(m.phase);
+    vec(m.decay_t);
+    vec(m.decay_s);
+    vec(m.shift_t);
+    vec(m.shift_s);
+  }
+  std::vector<unsigned char> take() { return std::move(b_); }
+
+ private:
+  std::vector<unsigned char> b_;
+};
+
+std::vector<unsigned char> content_key(const Periodizer& pz) {
+  Bytes k;
+  k.pod(pz.pde);
+  k.pod(pz.beta);
+  k.pod(pz.cell.d);
+  k.pod(pz.cell.xi);
+  k.pod(pz.cell.eta);
+  k.pod(pz.cell.periodicity);
+  k.pod(pz.cell.m0);
+  k.pod(pz.eps);
+  k.pod(pz.dlp);
+  k.pod(pz.multipole_order);
+  k.pod(pz.requires_neutrality);
+  k.pod(pz.scalar_parts.size());
+  for (const auto& p : pz.scalar_parts) {
+    k.pod(p.dir);
+    k.modes(p.modes);
+    k.vec(p.diag);
+    k.pod(p.take_real);
+    k.pod(p.has_m0);
+    k.pod(p.m0_coef);
+  }
+  k.pod(pz.block_parts.size());
+  for (const auto& p : pz.block_parts) {
+    k.pod(p.dir);
+    k.modes(p.modes);
+    k.vec(p.diag_a);
+    k.vec(p.diag_b);
+    k.pod(p.three_term);
+    k.pod(p.take_real);
+    k.pod(p.has_m0);
+    k.pod(p.m0_mat);
+  }
+  k.pod(pz.pressure_parts.size());
+  for (const auto& p : pz.pressure_parts) {
+    k.pod(p.dir);
+    k.modes(p.modes);
+    k.vec(p.diag);
+    k.vec(p.row);
+    k.pod(p.has_m0);
+    k.pod(p.m0_coef);
+    k.pod(p.m0_row);
+  }
+  k.pod(pz.stresslet_parts.size());
+  for (const auto& p : pz.stresslet_parts) {
+    k.pod(p.dir);
+    k.modes(p.modes);
+    k.vec(p.a1);
+    k.vec(p.a2);
+    k.vec(p.smat);
+    k.vec(p.sa);
+    k.vec(p.sb);
+    k.vec(p.off);
+    k.pod(p.has_m0);
+    k.pod(p.m0_coef);
+  }
+  return k.take();
+}
+
+class PlanCache {
+ public:
+  static PlanCache& instance() {
+    static PlanCache* c = new PlanCache;  // never destroyed (see above)
+    return *c;
+  }
+  std::shared_ptr<pwb_periodizer> get(const Periodizer& pz) {
+    std::vector<unsigned char> key = content_key(pz);
+    std::lock_guard<std::mutex> g(mu_);
+    ++tick_;
+    for (auto& e : entries_)
+      if (e.key == key) {
+        e.last = tick_;
+        return e.h;
+      }
+    if (entries_.size() >= capacity()) {
+      auto lru = std::min_element(entries_.begin(), entries_.end(),
+                                  [](const Entry& a, const Entry& b) { return a.last < b.last; });
+      entries_.erase(lru);  // freed when the last call using it returns
+    }
+    entries_.push_back(Entry{std::move(key), std::shared_ptr<pwb_periodizer>(pwb::wrap_periodizer(pz),
+                                                                             pwb_periodizer_free),
+                             tick_});
+    return entries_.back().h;
+  }
+ private:
+  struct Entry {
+    std::vector<unsigned char> key;
+    std::shared_ptr<pwb_periodizer> h;
+    unsigned long long last;
+  };
+  static size_t capacity() {
+    const char* e = std::getenv("PWB_PLAN_CACHE");
+    const long v = e ? std::strtol(e, nullptr, 10) : 8;
+    return static_cast<size_t>(std::max(1L, v));
+  }
+  std::mutex mu_;
+  std::vector<Entry> entries_;
+  unsigned long long tick_ = 0;
+};
+
+// The cached handle of `pz` (shared between calls with equal periodizers).
 struct Handle {
+  std::shared_ptr<pwb_periodizer> keep;
   pwb_periodizer* h;
-  explicit Handle(const Periodizer& pz) : h(pwb::wrap_periodizer(pz)) {}
-  ~Handle() { pwb_periodizer_free(h); }
+  explicit Handle(const Periodizer& pz) : keep(PlanCache::instance().get(pz)), h(keep.get()) {}
 };
 
 pwb_system system_of(const ParticleSystem& s) {

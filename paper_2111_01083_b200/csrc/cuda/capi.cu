@@ -147,9 +147,13 @@ void stage_in(pwb::Plan& p, const pwb_system* s, cudaStream_t st, pwb::DevSys* d
   ds->f = put(p.stage[2], s->forces, 2 * s->n_src, st);
   ds->nrm = put(p.stage[3], s->normals, 2 * s->n_src, st);
   ds->coef = put(p.stage[4], s->coefficients, 2 * s->n_src, st);
-  // targets given as the sources array itself: keep them one device array so the
-  // symmetric near tile (every unordered pair once) applies
-  if (s->targets == s->sources && s->n_tgt == s->n_src)
+  // targets given as the sources array itself, or as a separate host array holding the
+  // same bytes (the reference's ParticleSystem keeps two vectors, cell.hpp:58-65, so a
+  // drop-in caller with targets = sources passes a copy): keep them one device array so the
+  // symmetric near tile (every unordered pair once) applies. Equal bytes are equal points
+  // (one O(N) memcmp, against O(N^2) pair work), so the result is the aliased call's.
+  if (s->n_tgt == s->n_src && s->targets &&
+      (s->targets == s->sources || std::memcmp(s->targets, s->sources, 2 * s->n_src * sizeof(double)) == 0))
     ds->tgt = ds->src;
   else
     ds->tgt = put(p.stage[5], s->targets, 2 * s->n_tgt, st);

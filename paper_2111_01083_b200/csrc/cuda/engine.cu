@@ -23,9 +23,11 @@ void throw_internal(const char* what) { throw InternalFailure(what); }
 
 namespace {
 std::atomic<long> g_launches{0};
+std::atomic<unsigned long> g_buffer_epoch{0};
 }
 void count_launches(long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+unsigned long buffer_epoch() { return g_buffer_epoch.load(std::memory_order_acquire); }
 
 DevBuf::~DevBuf() {
   if (p_) cudaFree(p_);
@@ -37,6 +39,7 @@ void* DevBuf::ensure(size_t bytes) {
     if (p_) cuda_check(cudaFree(p_), "cudaFree");
     p_ = nullptr;
     n_ = 0;
+    g_buffer_epoch.fetch_add(1, std::memory_order_acq_rel);
     cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
     n_ = bytes;
   }
@@ -53,6 +56,7 @@ void* PinnedBuf::ensure(size_t bytes) {
     if (p_) cuda_check(cudaFreeHost(p_), "cudaFreeHost");
     p_ = nullptr;
     n_ = 0;
+    g_buffer_epoch.fetch_add(1, std::memory_order_acq_rel);
     cuda_check(cudaMallocHost(&p_, bytes), "cudaMallocHost");
     n_ = bytes;
   }
@@ -169,6 +173,9 @@ Plan::~Plan() {
   if (cudaGetDevice(&restore_.prev) != cudaSuccess) restore_.prev = -1;
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);  // nothing in flight when the FFT plans and buffers go
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (capture_stream_) cudaStreamDestroy(capture_stream_);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
@@ -542,20 +549,32 @@ void Plan::validate(const DevSys& s, const Opts& o, bool far_checks, bool neutra
   launch_reduce(ra, bm, bc, st);
   launch_sum_blocks(bc, kReduceBlocks, kChecks, outv + kMoments, st);
   cuda_check(cudaGetLastError(), "validate launch");
-  double* h = static_cast<double*>(host_checks_.ensure(64 * sizeof(double)));
-  cuda_check(cudaMemcpyAsync(h, outv + kMoments, kChecks * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H checks");
+  const double* h = static_cast<double*>(host_checks_.ensure(64 * sizeof(double)));
+  cuda_check(cudaMemcpyAsync(const_cast<double*>(h), outv + kMoments, kChecks * sizeof(double), cudaMemcpyDeviceToHost,
+                             st),
+             "D2H checks");
+  const bool neutral = pz_.requires_neutrality && neutrality;
+  auto check = [h, far_checks, neutral, kind] {
+    if (far_checks)
+      require(h[0] == 0.0, ErrorCode::OutOfInterval, "source or target point outside the closed unit cell");
+    require(h[1] == 0.0, ErrorCode::NonUnitNormal, "stresslet normals must be unit vectors");
+    if (!neutral) return;  // apply.cpp:365-392
+    if (kind == Kind::Multipole)
+      require(std::hypot(h[7], h[8]) <= 1e-12 * h[9], ErrorCode::NotNeutral,
+              "this periodizer requires coefficients summing to zero");
+    else if (kind == Kind::Velocity)
+      require(std::hypot(h[4], h[5]) <= 1e-12 * h[6], ErrorCode::NotNeutral,
+              "this periodizer requires forces summing to zero");
+    else
+      require(std::abs(h[2]) <= 1e-12 * h[3], ErrorCode::NotNeutral,
+              "this periodizer requires charges summing to zero");
+  };
+  if (defer_) {
+    pending_.push_back(check);
+    return;
+  }
   cuda_check(cudaStreamSynchronize(st), "validate sync");
-  if (far_checks) require(h[0] == 0.0, ErrorCode::OutOfInterval, "source or target point outside the closed unit cell");
-  require(h[1] == 0.0, ErrorCode::NonUnitNormal, "stresslet normals must be unit vectors");
-  if (!pz_.requires_neutrality || !neutrality) return;  // apply.cpp:365-392
-  if (kind == Kind::Multipole)
-    require(std::hypot(h[7], h[8]) <= 1e-12 * h[9], ErrorCode::NotNeutral,
-            "this periodizer requires coefficients summing to zero");
-  else if (kind == Kind::Velocity)
-    require(std::hypot(h[4], h[5]) <= 1e-12 * h[6], ErrorCode::NotNeutral,
-            "this periodizer requires forces summing to zero");
-  else
-    require(std::abs(h[2]) <= 1e-12 * h[3], ErrorCode::NotNeutral, "this periodizer requires charges summing to zero");
+  check();
 }
 
 SpreadArgs Plan::vert_spread_args(const DevSys& s, bool sources) const {
@@ -1121,7 +1140,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   // one-sided tile with source splits is faster there)
   const bool symmetric = !single && s.tgt == s.src && s.nt == s.ns && s.nt >= 32768 && near_sym_supported(nk) &&
                          std::getenv("PWB_NO_SYMMETRIC") == nullptr;
-  cuda_check(cudaEventRecord(ev_[2], st), "event");
+  record(2, st);
   // screened kernels branch on beta*r per pair: bin so the branch is warp-uniform
   const bool screened = near_screened(nk, a);
   if (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)
@@ -1141,11 +1160,21 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
     double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
     launch_near(nk, a, st, ws, sms_);
   }
-  cuda_check(cudaEventRecord(ev_[3], st), "event");
+  record(3, st);
   near_timed_ = true;
   cuda_check(cudaGetLastError(), "near launch");
-  int* hflag = static_cast<int*>(host_checks_.ensure(64 * sizeof(double)));
+  // the flag lands past validate's check words (a deferred call still reads those)
+  int* hflag = reinterpret_cast<int*>(static_cast<double*>(host_checks_.ensure(64 * sizeof(double))) + 56);
   cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+  if (defer_) {
+    // deferred calls are one-sided (graph_eligible): no fixed-point fallback to run
+    require(!symmetric, ErrorCode::Unsupported, "internal: symmetric tile in a deferred call");
+    pending_.push_back([hflag] {
+      require((*hflag & 1) == 0, ErrorCode::CoincidentSourceTarget,
+              "a target coincides with a lattice image of a source");
+    });
+    return;
+  }
   cuda_check(cudaStreamSynchronize(st), "near sync");
   require((*hflag & 1) == 0, ErrorCode::CoincidentSourceTarget, "a target coincides with a lattice image of a source");
   if (*hflag & 2) {
@@ -1163,7 +1192,124 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   }
 }
 
+void Plan::record(int i, cudaStream_t st) {
+  // inside a capture the event becomes a graph node that records on every replay
+  if (defer_)
+    cuda_check(cudaEventRecordWithFlags(ev_[i], st, cudaEventRecordExternal), "event");
+  else
+    cuda_check(cudaEventRecord(ev_[i], st), "event");
+}
+
+bool Plan::GraphKey::operator==(const GraphKey& o) const {
+  return s.src == o.s.src && s.q == o.s.q && s.f == o.s.f && s.nrm == o.s.nrm && s.coef == o.s.coef &&
+         s.ns == o.s.ns && s.tgt == o.s.tgt && s.nt == o.s.nt && out.scalar == o.out.scalar &&
+         out.velocity == o.out.velocity && out.pressure == o.out.pressure &&
+         out.complex_scalar == o.out.complex_scalar && out.gradient == o.out.gradient && path == o.path &&
+         pressure == o.pressure && gradient == o.gradient && far == o.far && near == o.near &&
+         nufft_eps == o.nufft_eps;
+}
+
+// Launch-latency-bound calls only: both passes, one-sided near tile (the symmetric tile
+// needs n >= 32768 and may fall back on a status word), at most ~4M pairs.
+bool Plan::graph_eligible(const DevSys& s, bool far, bool near_images) const {
+  static const bool off = std::getenv("PWB_NO_GRAPH") != nullptr;
+  return !off && far && near_images && s.ns > 0 && s.nt > 0 && s.nt < 32768 &&
+         static_cast<double>(s.ns) * static_cast<double>(s.nt) <= 4.2e6;
+}
+
+void Plan::drop_graphs() {
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  graphs_.clear();
+  seen_.clear();
+}
+
 bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
+  if (graph_eligible(s, far, near_images)) return total_graphed(s, o, out, far, near_images);
+  return total_eager(s, o, out, far, near_images);
+}
+
+bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
+  GraphKey k;
+  k.s = s;
+  k.out = out;
+  k.path = static_cast<int>(o.path);
+  k.pressure = o.with_pressure;
+  k.gradient = o.with_gradient;
+  k.far = far;
+  k.near = near_images;
+  k.nufft_eps = o.nufft_eps;
+  if (graph_epoch_ != buffer_epoch()) {  // a workspace moved: every captured graph is stale
+    drop_graphs();
+    graph_epoch_ = buffer_epoch();
+  }
+  cudaStream_t st = stream_for(o);
+  auto launch = [&](const GraphEntry& e) {
+    cuda_check(cudaGraphLaunch(e.exec, st), "graph launch");
+    count_launches(e.launches);
+    cuda_check(cudaStreamSynchronize(st), "graph sync");
+    far_timed_ = e.far_timed;
+    near_timed_ = e.near_timed;
+    for (const auto& c : e.checks) c();
+    return e.accelerated;
+  };
+  for (const auto& e : graphs_)
+    if (e.key == k) return launch(e);
+  if (std::find(seen_.begin(), seen_.end(), k) == seen_.end()) {
+    // first sighting: run eagerly (sizes every workspace and one-time setup), remember it
+    const bool acc = total_eager(s, o, out, far, near_images);
+    if (seen_.size() >= 16) seen_.erase(seen_.begin());
+    seen_.push_back(k);
+    graph_epoch_ = buffer_epoch();
+    return acc;
+  }
+  // second sighting: capture the whole call on the plan's capture stream, replay on `st`
+  if (!capture_stream_) cuda_check(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking), "stream");
+  Opts oc = o;
+  oc.stream = capture_stream_;
+  GraphEntry e;
+  e.key = k;
+  const long l0 = launch_count();
+  cuda_check(cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  defer_ = true;
+  pending_.clear();
+  cudaGraph_t graph = nullptr;
+  try {
+    e.accelerated = total_eager(s, oc, out, far, near_images);
+  } catch (...) {
+    defer_ = false;
+    cudaStreamEndCapture(capture_stream_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    pending_.clear();
+    throw;
+  }
+  defer_ = false;
+  cuda_check(cudaStreamEndCapture(capture_stream_, &graph), "end capture");
+  e.launches = launch_count() - l0;
+  count_launches(-e.launches);  // captured, not run: counted on every replay instead
+  e.far_timed = far_timed_;
+  e.near_timed = near_timed_;
+  e.checks = std::move(pending_);
+  pending_.clear();
+  cudaError_t err = cudaGraphInstantiate(&e.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  cuda_check(err, "graph instantiate");
+  if (graph_epoch_ != buffer_epoch()) {  // the capture itself grew a workspace: replay later
+    cudaGraphExecDestroy(e.exec);
+    graph_epoch_ = buffer_epoch();
+    drop_graphs();
+    return total_eager(s, o, out, far, near_images);
+  }
+  if (graphs_.size() >= 8) {
+    cudaGraphExecDestroy(graphs_.front().exec);
+    graphs_.erase(graphs_.begin());
+  }
+  graphs_.push_back(std::move(e));
+  return launch(graphs_.back());
+}
+
+bool Plan::total_eager(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
   bool accelerated = false;
   cudaStream_t st = stream_for(o);
   far_timed_ = near_timed_ = false;
@@ -1171,10 +1317,10 @@ bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bo
     validate(s, o, true);
     const periwave::ApplyPath path = resolve(o, s.ns, s.nt);
     double* coeff = coeff_ws_.as<double>(coeff_size(o, path));
-    cuda_check(cudaEventRecord(ev_[0], st), "event");
+    record(0, st);
     source_pass(s, o, coeff, path);
     accelerated = target_pass(s, o, coeff, out, path);
-    cuda_check(cudaEventRecord(ev_[1], st), "event");
+    record(1, st);
     far_timed_ = true;
   }
   if (near_images) {

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -30,6 +31,10 @@ class FftPlans {
  private:
   std::map<std::pair<int, int>, int> plans_;  // cufftHandle is an int
 };
+
+// Bumped whenever a DevBuf / PinnedBuf moves (grows): captured CUDA graphs hold raw
+// workspace pointers and are dropped when it changes (Plan::total_graphed).
+unsigned long buffer_epoch();
 
 // RAII device buffer that only grows.
 class DevBuf {
@@ -185,7 +190,9 @@ class Plan {
   // item boundaries [world + 1] of a balanced multi-GPU split of the symmetric items
   void sym_split(const DevSys& s, const Opts& o, int world, long* bounds);
   void fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, int scale_exp, const DevOut& out);
-  // full pipeline on device pointers; returns the accelerated flag
+  // full pipeline on device pointers; returns the accelerated flag. Small one-sided
+  // problems replay a captured CUDA graph of the whole sequence (validation reductions,
+  // far passes, near tile, status copies) with one host synchronisation.
   bool total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images);
 
   std::mutex& mutex() { return mu_; }
@@ -220,6 +227,37 @@ class Plan {
   std::mutex mu_;
   cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
   bool far_timed_ = false, near_timed_ = false;
+
+  // ---- CUDA-graph replay of small calls (launch-latency bound: c1 is 15 launches of a
+  // few microseconds each). A call shape (every pointer, size and option) seen twice is
+  // captured once; the validation and coincidence checks are deferred to after the
+  // single synchronisation (the call still raises; outputs are unspecified on error).
+  struct GraphKey {
+    DevSys s;
+    DevOut out;
+    int path = 0;
+    bool pressure = false, gradient = false, far = false, near = false;
+    double nufft_eps = 0.0;
+    bool operator==(const GraphKey& o) const;
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    long launches = 0;
+    bool accelerated = false, far_timed = false, near_timed = false;
+    std::vector<std::function<void()>> checks;
+  };
+  bool graph_eligible(const DevSys& s, bool far, bool near_images) const;
+  bool total_eager(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images);
+  bool total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images);
+  void drop_graphs();
+  void record(int i, cudaStream_t st);
+  bool defer_ = false;                          // checks go to pending_ instead of syncing
+  std::vector<std::function<void()>> pending_;  // deferred checks of the call being captured
+  std::vector<GraphEntry> graphs_;
+  std::vector<GraphKey> seen_;
+  unsigned long graph_epoch_ = 0;
+  cudaStream_t capture_stream_ = nullptr;
 
   VertAccel va_;
   HorizAccel ha_;

@@ -1,0 +1,149 @@
+// Drop-in check and timer: the reference's own call shape against the C-ABI fast path.
+//
+//   pwb-dropin-bench PDE BETA D XI ETA PERIODICITY EPS INPUTS.bin OUT_PREFIX [REPS]
+//
+// INPUTS.bin: uint64 n, uint64 w (1 = charges, 2 = forces), 2n doubles sources, w*n
+// doubles strengths. Targets = sources.
+//
+// (1) periwave::total_field(pz, sys) exactly as a reference user calls it
+//     (proj/include/periwave/apply.hpp:58-60): a fresh ParticleSystem whose `targets` is a
+//     separate std::vector holding a copy of `sources` (cell.hpp:58-65), the periodizer by
+//     const&, host vectors in and out. Timed per call (wall clock, host to host).
+// (2) pwb_total_field through the C-ABI with targets == sources (one host pointer), the
+//     path the headline bench line takes with host buffers.
+// Writes OUT_PREFIX.dropin.bin / OUT_PREFIX.capi.bin (the output doubles) and prints one
+// JSON line with the per-call times. The first call of each arm is the warm-up (plan
+// upload) and is reported apart.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "periwave/periwave.hpp"
+#include "periwave_b200.h"
+
+namespace {
+
+double now_ms() {
+  using C = std::chrono::steady_clock;
+  return std::chrono::duration<double, std::milli>(C::now().time_since_epoch()).count();
+}
+
+double median(std::vector<double> v) {
+  std::sort(v.begin(), v.end());
+  return v.empty() ? 0.0 : v[v.size() / 2];
+}
+
+void write(const std::string& path, const double* p, size_t n) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f || std::fwrite(p, sizeof(double), n, f) != n) {
+    std::fprintf(stderr, "cannot write %s\n", path.c_str());
+    std::exit(3);
+  }
+  std::fclose(f);
+}
+
+std::string list(const std::vector<double>& v) {
+  std::string s = "[";
+  for (size_t i = 0; i < v.size(); ++i) s += (i ? ", " : "") + std::to_string(v[i]);
+  return s + "]";
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 10) {
+    std::fprintf(stderr, "usage: %s PDE BETA D XI ETA PERIODICITY EPS INPUTS.bin OUT_PREFIX [REPS]\n", argv[0]);
+    return 2;
+  }
+  const int pde = std::atoi(argv[1]);
+  const double beta = std::atof(argv[2]), d = std::atof(argv[3]), xi = std::atof(argv[4]), eta = std::atof(argv[5]);
+  const int per = std::atoi(argv[6]);
+  const double eps = std::atof(argv[7]);
+  const std::string out_prefix = argv[9];
+  const int reps = argc > 10 ? std::atoi(argv[10]) : 5;
+
+  FILE* f = std::fopen(argv[8], "rb");
+  uint64_t hdr[2];
+  if (!f || std::fread(hdr, sizeof(uint64_t), 2, f) != 2) {
+    std::fprintf(stderr, "cannot read %s\n", argv[8]);
+    return 2;
+  }
+  const size_t n = hdr[0], w = hdr[1];
+  std::vector<double> pts(2 * n), str(w * n);
+  if (std::fread(pts.data(), sizeof(double), pts.size(), f) != pts.size() ||
+      std::fread(str.data(), sizeof(double), str.size(), f) != str.size()) {
+    std::fprintf(stderr, "short read %s\n", argv[8]);
+    return 2;
+  }
+  std::fclose(f);
+
+  try {
+    // ---- (1) the reference's call shape
+    const periwave::UnitCell cell =
+        periwave::make_unit_cell(d, xi, eta, per == 1 ? periwave::Periodicity::Singly : periwave::Periodicity::Doubly);
+    const periwave::Periodizer pz = periwave::make_periodizer(static_cast<periwave::Pde>(pde), beta, cell, eps);
+    std::vector<double> dropin_ms;
+    periwave::FieldResult res;
+    for (int r = 0; r <= reps; ++r) {
+      periwave::ParticleSystem sys;  // rebuilt per call, as a caller with fresh data would
+      sys.sources.resize(n);
+      for (size_t i = 0; i < n; ++i) sys.sources[i] = {pts[2 * i], pts[2 * i + 1]};
+      if (w == 1) {
+        sys.charges = str;
+      } else {
+        sys.forces.resize(n);
+        for (size_t i = 0; i < n; ++i) sys.forces[i] = {str[2 * i], str[2 * i + 1]};
+      }
+      sys.targets = sys.sources;  // a separate vector: equal bytes, distinct storage
+      const double t0 = now_ms();
+      res = periwave::total_field(pz, sys);
+      dropin_ms.push_back(now_ms() - t0);
+    }
+    const bool vel = !res.velocity.empty();
+    const size_t nout = vel ? 2 * n : n;
+    write(out_prefix + ".dropin.bin", vel ? reinterpret_cast<const double*>(res.velocity.data()) : res.scalar.data(),
+          nout);
+
+    // ---- (2) the C-ABI with one host array for sources and targets
+    pwb_cell c;
+    if (pwb_make_unit_cell(d, xi, eta, per, &c) != PWB_OK) throw std::runtime_error(pwb_last_error());
+    pwb_periodizer* h = nullptr;
+    if (pwb_make_periodizer(pde, beta, &c, eps, &h) != PWB_OK) throw std::runtime_error(pwb_last_error());
+    pwb_system s{};
+    s.n_src = s.n_tgt = n;
+    s.sources = s.targets = pts.data();
+    (w == 1 ? s.charges : s.forces) = str.data();
+    s.memory = PWB_MEM_HOST;
+    pwb_options o;
+    pwb_options_default(&o);
+    std::vector<double> out(nout);
+    pwb_field fo{};
+    (vel ? fo.velocity : fo.scalar) = out.data();
+    fo.memory = PWB_MEM_HOST;
+    std::vector<double> capi_ms;
+    for (int r = 0; r <= reps; ++r) {
+      const double t0 = now_ms();
+      if (pwb_total_field(h, &s, &o, &fo) != PWB_OK) throw std::runtime_error(pwb_last_error());
+      capi_ms.push_back(now_ms() - t0);
+    }
+    write(out_prefix + ".capi.bin", out.data(), nout);
+    pwb_periodizer_free(h);
+
+    const double first_dropin = dropin_ms.front(), first_capi = capi_ms.front();
+    dropin_ms.erase(dropin_ms.begin());
+    capi_ms.erase(capi_ms.begin());
+    std::printf(
+        "{\"n\": %zu, \"reps\": %d, \"dropin_ms\": %s, \"capi_ms\": %s, \"dropin_median_ms\": %.3f, "
+        "\"capi_median_ms\": %.3f, \"dropin_first_ms\": %.3f, \"capi_first_ms\": %.3f}\n",
+        n, reps, list(dropin_ms).c_str(), list(capi_ms).c_str(), median(dropin_ms), median(capi_ms), first_dropin,
+        first_capi);
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+  return 0;
+}

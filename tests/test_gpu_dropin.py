@@ -1,0 +1,58 @@
+"""The drop-in C++ API at headline speed (compiled: csrc/tools/pwb_dropin_bench.cpp).
+
+A reference user calls periwave::total_field(pz, sys) with `sys.targets` a separate vector
+holding the sources (proj/include/periwave/apply.hpp:58-60, cell.hpp:58-65). That call must
+reach the same symmetric tile as the C-ABI with one array (bitwise equal outputs) and
+cost the same: the device plan is cached per periodizer content (api.cu PlanCache) and the
+host staging aliases byte-equal targets to the sources (capi.cu stage_in)."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+BIN = os.path.join(ROOT, "paper_2111_01083_b200", "bin", "pwb-dropin-bench")
+
+
+def _run(name, tmp_path, n=None, reps=3):
+    from paper_2111_01083_b200 import configs
+
+    inp = configs.generate(name, n_src=n)
+    c = inp.config
+    s = inp.charges if c.strength == "charge" else inp.forces
+    w = 1 if c.strength == "charge" else 2
+    path = tmp_path / f"{name}.bin"
+    with open(path, "wb") as f:
+        f.write(np.array([len(inp.sources), w], dtype=np.uint64).tobytes())
+        f.write(np.ascontiguousarray(inp.sources).tobytes())
+        f.write(np.ascontiguousarray(s).tobytes())
+    d, xi, eta, per = c.cell
+    out = tmp_path / name
+    r = subprocess.run([BIN, str(int(c.pde)), repr(c.beta), repr(d), repr(xi), repr(eta), str(int(per)), repr(c.eps),
+                        str(path), str(out), str(reps)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    a = np.fromfile(f"{out}.dropin.bin", dtype=np.float64)
+    b = np.fromfile(f"{out}.capi.bin", dtype=np.float64)
+    return line, a, b
+
+
+@pytest.mark.parametrize("name", ["c4", "c3"])
+def test_dropin_total_field_is_the_capi_fast_path(gpu, tmp_path, name):
+    line, a, b = _run(name, tmp_path)
+    assert np.array_equal(a, b)
+    # same tile, same staging: the reference-shaped call costs what the C-ABI call costs
+    assert line["dropin_median_ms"] <= 1.05 * line["capi_median_ms"] + 2.0, line
+    print(json.dumps({"config": name, **line}))
+
+
+def test_dropin_small_system_reuses_the_plan(gpu, tmp_path):
+    """c1-sized calls: after the first call no per-call plan build (the old per-call Handle
+    cost a stream, table upload and workspaces every time)."""
+    line, a, b = _run("c1", tmp_path, reps=20)
+    assert np.array_equal(a, b)
+    assert line["dropin_median_ms"] < 0.25 * line["dropin_first_ms"], line
