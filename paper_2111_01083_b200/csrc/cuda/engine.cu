@@ -943,6 +943,12 @@ NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool
     // round x_c^2 up to a zero low word: the tiles compare high words on the integer pipe
     // (pw_math.cuh lt_hi), exact for such a bound
     a.xcut2 = pwk::hi_lo(pwk::hi_of(xc * xc) + (pwk::lo_of(xc * xc) != 0u ? 1 : 0), 0u);
+    // per-tile-pair Chebyshev K0 of the symmetric tile (pw_math.cuh cheb_fit_k0): relative
+    // error <= 1e-3 eps per pair, in the coarse tier (eps >= 1e-10); PWB_NO_CHEB: off (A/B)
+    if (nk == NearKind::ModHelm && a.lowp == 2 && std::getenv("PWB_NO_CHEB") == nullptr) {
+      a.cheb_tol = 1e-3 * pz_.eps;
+      a.inv_beta2 = 1.0 / a.beta2;
+    }
   }
   return nk;
 }

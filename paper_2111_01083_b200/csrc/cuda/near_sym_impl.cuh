@@ -200,6 +200,7 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool FAST = false, LOWP = LOWP_;
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
+  static constexpr bool CHEB = !GRAD;     // regime 3: per-tile-pair Chebyshev K0 (pw_math.cuh cheb_fit_k0)
   static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
@@ -610,10 +611,19 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         const double shx = a.shx[img], shy = a.shy[img / NXI];
         const bool ident = img == a.id_img;
         int regime = 0;  // per-pair dispatch unless the boxes pin the whole tile pair
+        pwk::ChebFit<kChebDeg> cf;
         if (a.cull) {
           double lo, hi;
           image_xrange(rb, cbx, shx, shy, a.beta2, lo, hi);
           regime = pwk::regime_of(lo, hi, a.xcut2);
+          if constexpr (K::CHEB) {
+            // regime 3: the tile pair's s = r^2 interval is short enough for one fitted
+            // polynomial (block-uniform: every warp fits the same interval identically).
+            // x >= 0.5 keeps it clear of the log singularity and of any exact zero.
+            if (a.cheb_tol > 0.0 && lo * 0.9999 > 0.25 &&
+                pwk::cheb_fit_k0(lo * 0.9999, hi * 1.0001, a.beta2, a.inv_beta2, a.cheb_tol, cf))
+              regime = 3;
+          }
         }
         auto sweep = [&](auto reg) {
           constexpr int R = decltype(reg)::value;
@@ -645,6 +655,8 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
               const double ry = R == 0 ? (ty[k] - sy) - shy : tys[k] - sy;
               if constexpr (R == 0) {
                 if (!K::image_value(V, rx, ry, ident, a, flag)) continue;
+              } else if constexpr (R == 3) {
+                V[0] = pwk::cheb_eval(cf, rx, ry);
               } else {
                 K::template image_fast<R == 2>(V, rx, ry, a);
               }
@@ -655,6 +667,12 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
             for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
           }
         };
+        if constexpr (K::CHEB) {
+          if (regime == 3) {
+            sweep(std::integral_constant<int, 3>{});
+            continue;
+          }
+        }
         if (regime == 2)
           sweep(std::integral_constant<int, 2>{});
         else if (regime == 1 && PWB_SYM_MH_NEAR_SWEEP)

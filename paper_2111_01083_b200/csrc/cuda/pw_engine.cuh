@@ -86,6 +86,8 @@ struct NearArgs {
   int cull = 1;                  // screened symmetric tiles: per-tile image mask (near_sym_impl.cuh)
   int unskewed = 0;              // fused layout with shx[n][m] independent of n (xi == 0)
   int coarse_log = 0;            // symmetric Laplace / Stokeslet tiles: 256-entry table log (eps >= 1e-10)
+  double cheb_tol = 0.0;         // screened symmetric tile: per-tile-pair Chebyshev K0 fit (0: off)
+  double inv_beta2 = 0.0;
 };
 
 // ---------------------------------------------------------------- spatial binning (binning.cu)

@@ -382,6 +382,7 @@ def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad, sym, cellt,
     # eps 1e-8: reduced / coarse Bessel tiers; 1e-12: the full tier
     pz = pw.make_periodizer(pw.Pde.ModHelmholtz, beta, _cell(pw, cellt), eps)
     s = pw.ParticleSystem(sources=src, targets=src if sym else src.copy(), charges=q)
+    monkeypatch.setenv("PWB_NO_CHEB", "1")  # the fitted regime approximates K0 (tested below)
     culled = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
     monkeypatch.setenv("PWB_NO_CULL", "1")
     full = pw.near_field(pz, s, pw.ApplyOptions(with_gradient=grad))
@@ -389,6 +390,39 @@ def test_screened_image_culling_is_exact(pw, gpu, monkeypatch, grad, sym, cellt,
     assert np.max(np.abs(culled.scalar - full.scalar)) <= 1e-14 * np.max(np.abs(full.scalar))
     if grad:
         assert np.max(np.abs(culled.gradient - full.gradient)) <= 1e-14 * np.max(np.abs(full.gradient))
+
+
+@pytest.mark.parametrize("cellt,beta,n,fits", [((4.0, 0.0, 1.0, 2), 1.0, 200000, True),
+                                               ((1.0, 0.3, 0.8, 2), 2.0, 200000, False)])
+def test_screened_chebyshev_regime(pw, gpu, ref, monkeypatch, cellt, beta, n, fits):
+    """Regime 3 of the screened symmetric tile (pw_math.cuh cheb_fit_k0): a tile pair whose
+    r^2 interval is short gets one degree-8 Chebyshev fit of K0 and every pair a Horner
+    step. Accepted fits bound the relative error per pair by 1e-3 eps; against the tile
+    without it (PWB_NO_CHEB: coarse asymptotic tier, ~1e-11) the near field agrees to
+    ~1e-3 eps, and the fitted regime did run (the results are not bitwise equal). Dense
+    points (c5's density is 1e5 per unit area) so the Morton tiles are small."""
+    rng = np.random.default_rng(2024)
+    d, xi, eta = cellt[:3]
+    u = rng.uniform(-0.5, 0.5, (n, 2))
+    src = np.ascontiguousarray(np.column_stack([u[:, 0] * d + u[:, 1] * xi, u[:, 1] * eta]))
+    q = np.ascontiguousarray(rng.standard_normal(n))
+    eps = 1e-8
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, beta, _cell(pw, cellt), eps)
+    s = pw.ParticleSystem(sources=src, targets=src, charges=q)
+    fit = pw.near_field(pz, s).scalar
+    monkeypatch.setenv("PWB_NO_CHEB", "1")
+    plain = pw.near_field(pz, s).scalar
+    if fits:  # c5-like: most tile pairs fit
+        assert not np.array_equal(fit, plain)
+    err = rel_l2(fit, plain)
+    print("chebyshev vs asymptotic tier rel l2", err)
+    assert err <= 1e-10
+    R = ref.make_periodizer(1, beta, tuple(float(v) for v in cellt[:3]) + (int(cellt[3]),), eps)
+    idx = rng.choice(n, 64, replace=False)
+    monkeypatch.delenv("PWB_NO_CHEB")
+    got = pw.total_field(pz, s, pw.ApplyOptions(path=pw.ApplyPath.Direct)).scalar
+    want = R.apply(0, src, np.ascontiguousarray(src[idx]), charges=q, path=1, threads=8)["scalar"]
+    assert rel_l2(got[idx], want) <= 10 * eps
 
 
 def test_symmetric_gradient_and_pressure(pw, gpu, ref):
