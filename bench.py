@@ -389,10 +389,13 @@ def main():
     dev_index = local % ngpu
     torch.cuda.set_device(dev_index)
     if sharded:
+        import datetime
+
+        tmo = datetime.timedelta(seconds=600)  # a dead rank fails the job instead of hanging it
         if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index), timeout=tmo)
         else:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=tmo)
     dev = torch.device("cuda", dev_index)
     stream = torch.cuda.current_stream()
 
@@ -474,12 +477,12 @@ def main():
     if sharded:
         tt = torch.zeros(ws, 3, dtype=torch.float64, device=dev)
         tt[rank] = torch.tensor([t_step, t_near, dev_index], dtype=torch.float64)
-        dist.all_reduce(tt)
+        comm.allreduce(tt)
         per_rank = [{"rank": r, "device": int(tt[r, 2]), "step_ms": float(tt[r, 0]), "near_ms": float(tt[r, 1]),
                      "far_ms": float(tt[r, 0] - tt[r, 1])} for r in range(ws)]
         t_step, t_near = float(tt[:, 0].max()), float(tt[:, 1].max())
         dg = torch.tensor(digest, dtype=torch.float64, device=dev)
-        dist.all_reduce(dg)
+        comm.allreduce(dg)
         digest = [float(v) for v in dg.tolist()]
 
     # ---- end to end through the public API from pinned host memory (H2D + compute + D2H)
@@ -511,7 +514,7 @@ def main():
     t_e2e = sum(e2e_ms) / len(e2e_ms)
     if sharded:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        comm.allreduce_max(tt)
         t_e2e = float(tt[0])
     nout = 1 if c.strength == "charge" else 2
     # bytes of the tensors copied per e2e step: sources + strengths (+ targets when separate)

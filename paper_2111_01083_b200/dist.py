@@ -38,6 +38,20 @@ def target_slice(n: int, world: int, rank: int):
     return lo, min(n, lo + c)
 
 
+def _host_staged(op, t):
+    """gloo reduces host tensors: a device tensor goes through a host copy (NCCL and host
+    tensors are reduced in place)."""
+    import torch.distributed as dist
+
+    if t.device.type == "cpu" or dist.get_backend() == "nccl":
+        op(t)
+        return t
+    h = t.cpu()
+    op(h)
+    t.copy_(h)
+    return t
+
+
 class Comm:
     """all_reduce / reduce_scatter (sum) over the default process group; world 1 is local."""
 
@@ -48,14 +62,14 @@ class Comm:
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(t)
+            _host_staged(dist.all_reduce, t)
         return t
 
     def allreduce_max(self, t):
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            _host_staged(lambda x: dist.all_reduce(x, op=dist.ReduceOp.MAX), t)
         return t
 
     def reduce_scatter(self, inp, out):
@@ -67,8 +81,8 @@ class Comm:
 
         if dist.get_backend() == "nccl":
             dist.reduce_scatter_tensor(out, inp)
-        else:  # gloo has no reduce-scatter: all-reduce then keep the own slice
-            tmp = inp.clone()
+        else:  # gloo has no reduce-scatter: all-reduce (on the host) then keep the own slice
+            tmp = inp.cpu() if inp.device.type != "cpu" else inp.clone()
             dist.all_reduce(tmp)
             r = dist.get_rank()
             out.copy_(tmp[r * out.numel():(r + 1) * out.numel()])

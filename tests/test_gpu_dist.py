@@ -42,8 +42,11 @@ def _worker(rank, world, port, outdir, name, n, coincident):
     import paper_2111_01083_b200 as pw
     from paper_2111_01083_b200 import dist as pdist
 
+    import datetime
+
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # a rank that dies must not leave its peer in a collective for gloo's 30-minute default
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=180))
     try:
         inp = _inputs(name, n, coincident)
         c = inp.config
