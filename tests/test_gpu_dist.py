@@ -29,8 +29,10 @@ def _inputs(name, n, coincident=False):
     from paper_2111_01083_b200 import configs
 
     inp = configs.generate(name, n_src=n)
-    if coincident:  # one source duplicated far down the list: one rank's items hold the pair
-        inp.sources[n - 3] = inp.sources[5]
+    if coincident:  # a source on the (1, 0) image of another, far down the list: one rank's items hold the pair
+        y = inp.sources[5, 1]
+        inp.sources[5] = (-0.5, y)
+        inp.sources[n - 3] = (0.5, y)
     return inp
 
 
