@@ -472,7 +472,11 @@ def main():
     t_step = sum(step_ms) / args.steps
     t_near = sum(near_ms) / args.steps
     res = out.scalar if out.scalar is not None else out.velocity
-    digest = [float(res.sum()), float((res * res).sum())]
+    # gauge-free digest (Poisson / Stokes fields are defined up to a constant per component,
+    # and the far field's reduction order moves that constant): per component sum, sum of
+    # squares, count -> centered l2
+    res2 = res.reshape(res.shape[0], -1)
+    digest = [float(v) for v in torch.cat([res2.sum(0), (res2 * res2).sum(0)]).tolist()] + [float(res2.shape[0])]
     per_rank = [{"rank": 0, "device": dev_index, "step_ms": t_step, "near_ms": t_near, "far_ms": t_step - t_near}]
     if sharded:
         tt = torch.zeros(ws, 3, dtype=torch.float64, device=dev)
@@ -559,7 +563,7 @@ def main():
                         "note": "ranks share GPUs (--dist-backend gloo): a functional run of the sharded "
                                 "path, not a scaling number" if shared else None},
             "per_rank": per_rank,
-            "output_digest": {"sum": digest[0], "l2": digest[1] ** 0.5},
+            "output_digest": output_digest(digest),
             "e2e": {"value": nt / (t_e2e * 1e-3), "unit": "targets/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
@@ -575,6 +579,15 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def output_digest(d):
+    """[sum_c..., sumsq_c..., n] over all ranks -> per-component mean and centered l2 norm
+    (sqrt(sum (u - mean)^2)): comparable across rank counts for every kernel."""
+    k = (len(d) - 1) // 2
+    n = d[-1]
+    return {"targets": int(n), "mean": [d[c] / n for c in range(k)],
+            "centered_l2": [max(0.0, d[k + c] - d[c] * d[c] / n) ** 0.5 for c in range(k)]}
 
 
 def ctypes_doubles():

@@ -46,10 +46,24 @@ class NearEvaluator : public periwave::FreeSpaceEvaluator {
                   bool identity_shift, const periwave::ApplyOptions& opt,
                   periwave::FieldResult& out) const override {
     std::lock_guard<std::mutex> g(mu_);
-    pwb_periodizer* h = handle(pz);
     const std::size_t ns = sys.sources.size(), nt = sys.targets.size();
     const bool multipole = pz.multipole_order >= 1;
     const bool velocity = !multipole && (pz.pde == periwave::Pde::Stokes || pz.pde == periwave::Pde::ModStokes);
+    // the strength lengths of check_strengths (apply.cpp:350-364): the C-ABI sees pointers only
+    using periwave::ErrorCode;
+    if (multipole)
+      periwave::require(sys.coefficients.size() == ns, ErrorCode::LengthMismatch,
+                        "multipole apply requires one complex coefficient per source");
+    else if (pz.dlp)
+      periwave::require(sys.forces.size() == ns && sys.normals.size() == ns, ErrorCode::LengthMismatch,
+                        "double-layer apply requires a force vector and a unit normal per source");
+    else if (velocity)
+      periwave::require(sys.forces.size() == ns, ErrorCode::LengthMismatch,
+                        "velocity apply requires one force vector per source");
+    else
+      periwave::require(sys.charges.size() == ns, ErrorCode::LengthMismatch,
+                        "scalar apply requires one charge per source");
+    pwb_periodizer* h = handle(pz);
     // ensure_sizes (apply.cpp:395-405): resize only when the length differs
     auto fit = [nt](auto& v) {
       if (v.size() != nt) v.assign(nt, typename std::decay_t<decltype(v)>::value_type{});

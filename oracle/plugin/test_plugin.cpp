@@ -69,16 +69,22 @@ std::string num(const char* k, double v) {
   return b;
 }
 
+// agreement bar: 1e-13 with the product's full precision tier (PWB_FULL_PRECISION=1, run with
+// argument "full"), else 1e-2 eps -- the reduced / coarse near-field tiers the product picks for
+// eps >= 1e-11 stay two orders below eps
+bool g_full = false;
+double bar(const Periodizer& pz) { return g_full ? 1e-13 : 1e-2 * pz.eps; }
+
 // total_field with the plug-in vs the stock evaluator: agreement, one call per image
-void compare(const std::string& name, const Periodizer& pz, const ParticleSystem& sys, const ApplyOptions& opt,
-             double tol) {
+void compare(const std::string& name, const Periodizer& pz, const ParticleSystem& sys, const ApplyOptions& opt) {
+  const double tol = bar(pz);
   periwave_b200::NearEvaluator gpu;
   const FieldResult a = total_field(pz, sys, opt, &gpu);
   const FieldResult b = total_field(pz, sys, opt);
   const int images = static_cast<int>(near_translations(pz.cell).size());
   const double e = rel(flat(a), flat(b));
   report(name, e <= tol && gpu.calls() == images && a.accelerated == b.accelerated,
-         num("rel_l2", e) + ", \"calls\": " + std::to_string(gpu.calls()) + ", \"images\": " + std::to_string(images));
+         num("rel_l2", e) + ", " + num("bar", tol) + ", \"calls\": " + std::to_string(gpu.calls()) + ", \"images\": " + std::to_string(images));
 }
 
 template <class F>
@@ -106,7 +112,7 @@ int run() {
     for (double& q : sys.charges) mean += (q = rng.uniform() * 2.0 - 1.0);
     for (double& q : sys.charges) q -= mean / 1000.0;
     sys.targets = sys.sources;
-    compare("c1_poisson_self", make_periodizer(Pde::Poisson, 0.0, cell, 1e-10), sys, {}, 1e-13);
+    compare("c1_poisson_self", make_periodizer(Pde::Poisson, 0.0, cell, 1e-10), sys, {});
   }
   {  // c2 shape: modified Helmholtz beta = 10 on the skewed cell, separate targets (m0 = 2)
     UnitCell cell = make_unit_cell(1.0, 0.3, 0.8, Periodicity::Doubly);
@@ -115,7 +121,7 @@ int run() {
     sys.targets = points(cell, rng, 1500);
     sys.charges.resize(2000);
     for (double& q : sys.charges) q = rng.uniform() * 2.0 - 1.0;
-    compare("c2_modhelm_skewed", make_periodizer(Pde::ModHelmholtz, 10.0, cell, 1e-10), sys, {}, 1e-13);
+    compare("c2_modhelm_skewed", make_periodizer(Pde::ModHelmholtz, 10.0, cell, 1e-10), sys, {});
   }
   {  // Stokes with pressure, singly periodic
     UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Singly);
@@ -128,7 +134,7 @@ int run() {
     for (auto& f : sys.forces) f = f - mean * (1.0 / 700.0);
     ApplyOptions opt;
     opt.with_pressure = true;
-    compare("stokes_pressure_singly", make_periodizer(Pde::Stokes, 0.0, cell, 1e-8), sys, opt, 1e-13);
+    compare("stokes_pressure_singly", make_periodizer(Pde::Stokes, 0.0, cell, 1e-8), sys, opt);
   }
   {  // empty target list: sizes follow ensure_sizes, no device work
     UnitCell cell = make_unit_cell(1.0, 0.0, 1.0, Periodicity::Doubly);
@@ -167,7 +173,8 @@ int run() {
   return failures ? 1 : 0;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  g_full = argc > 1 && std::string(argv[1]) == "full";
   try {
     return run();
   } catch (const std::exception& e) {

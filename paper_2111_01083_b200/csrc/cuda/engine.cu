@@ -1208,9 +1208,7 @@ void Plan::record(int i, cudaStream_t st) {
 
 bool Plan::GraphKey::operator==(const GraphKey& o) const {
   return s.src == o.s.src && s.q == o.s.q && s.f == o.s.f && s.nrm == o.s.nrm && s.coef == o.s.coef &&
-         s.ns == o.s.ns && s.tgt == o.s.tgt && s.nt == o.s.nt && out.scalar == o.out.scalar &&
-         out.velocity == o.out.velocity && out.pressure == o.out.pressure &&
-         out.complex_scalar == o.out.complex_scalar && out.gradient == o.out.gradient && path == o.path &&
+         s.ns == o.s.ns && s.tgt == o.s.tgt && s.nt == o.s.nt && outs == o.outs && path == o.path &&
          pressure == o.pressure && gradient == o.gradient && far == o.far && near == o.near &&
          nufft_eps == o.nufft_eps;
 }
@@ -1236,9 +1234,14 @@ bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bo
 }
 
 bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
+  // outputs: the graph writes the plan's own block (fixed pointers, so a caller that
+  // allocates fresh result arrays per call still replays) and every replay copies it out
+  double* const user[5] = {out.scalar, out.velocity, out.pressure, out.complex_scalar, out.gradient};
+  const size_t width[5] = {1, 2, 1, 2, 2};
   GraphKey k;
   k.s = s;
-  k.out = out;
+  for (int i = 0; i < 5; ++i)
+    if (user[i]) k.outs |= 1u << i;
   k.path = static_cast<int>(o.path);
   k.pressure = o.with_pressure;
   k.gradient = o.with_gradient;
@@ -1250,8 +1253,23 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
     graph_epoch_ = buffer_epoch();
   }
   cudaStream_t st = stream_for(o);
+  double* own[5] = {};
+  auto own_outputs = [&] {
+    double* base = graph_out_.as<double>(8 * s.nt);
+    size_t off = 0;
+    for (int i = 0; i < 5; ++i)
+      if (user[i]) {
+        own[i] = base + off;
+        off += width[i] * s.nt;
+      }
+  };
   auto launch = [&](const GraphEntry& e) {
+    own_outputs();
     cuda_check(cudaGraphLaunch(e.exec, st), "graph launch");
+    for (int i = 0; i < 5; ++i)
+      if (user[i])
+        cuda_check(cudaMemcpyAsync(user[i], own[i], width[i] * s.nt * sizeof(double), cudaMemcpyDeviceToDevice, st),
+                   "graph output copy");
     count_launches(e.launches);
     cuda_check(cudaStreamSynchronize(st), "graph sync");
     far_timed_ = e.far_timed;
@@ -1263,6 +1281,7 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
     if (e.key == k) return launch(e);
   if (std::find(seen_.begin(), seen_.end(), k) == seen_.end()) {
     // first sighting: run eagerly (sizes every workspace and one-time setup), remember it
+    own_outputs();  // size the output block now, so the capture does not move a buffer
     const bool acc = total_eager(s, o, out, far, near_images);
     if (seen_.size() >= 16) seen_.erase(seen_.begin());
     seen_.push_back(k);
@@ -1280,8 +1299,10 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
   defer_ = true;
   pending_.clear();
   cudaGraph_t graph = nullptr;
+  own_outputs();
+  const DevOut gout{own[0], own[1], own[2], own[3], own[4]};
   try {
-    e.accelerated = total_eager(s, oc, out, far, near_images);
+    e.accelerated = total_eager(s, oc, gout, far, near_images);
   } catch (...) {
     defer_ = false;
     cudaStreamEndCapture(capture_stream_, &graph);

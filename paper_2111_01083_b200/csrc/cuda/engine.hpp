@@ -234,7 +234,7 @@ class Plan {
   // single synchronisation (the call still raises; outputs are unspecified on error).
   struct GraphKey {
     DevSys s;
-    DevOut out;
+    unsigned outs = 0;  // which outputs are requested (bit i: scalar, velocity, pressure, complex, gradient)
     int path = 0;
     bool pressure = false, gradient = false, far = false, near = false;
     double nufft_eps = 0.0;
@@ -258,6 +258,7 @@ class Plan {
   std::vector<GraphKey> seen_;
   unsigned long graph_epoch_ = 0;
   cudaStream_t capture_stream_ = nullptr;
+  DevBuf graph_out_;  // the graph writes here; each replay copies into the caller's arrays
 
   VertAccel va_;
   HorizAccel ha_;

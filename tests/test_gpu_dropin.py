@@ -43,8 +43,13 @@ def _run(name, tmp_path, n=None, reps=3):
 
 @pytest.mark.parametrize("name", ["c4", "c3"])
 def test_dropin_total_field_is_the_capi_fast_path(gpu, tmp_path, name):
+    from conftest import rel_l2
+
     line, a, b = _run(name, tmp_path)
-    assert np.array_equal(a, b)
+    if name == "c3":  # Direct far field: the whole result is deterministic
+        assert np.array_equal(a, b)
+    else:  # c4's Auto path is the type-3 NUFFT (spreading sums in atomic order): ~1 ulp
+        assert rel_l2(a, b, gauge=True) <= 1e-14
     # same tile, same staging: the reference-shaped call costs what the C-ABI call costs
     assert line["dropin_median_ms"] <= 1.05 * line["capi_median_ms"] + 2.0, line
     print(json.dumps({"config": name, **line}))
