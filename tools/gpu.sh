@@ -10,17 +10,18 @@
 #   bench:CFG[:ARGS]    python bench.py --config CFG ARGS (ARGS: comma-separated flags)
 #   ref:CFG             python bench.py --impl reference --config CFG
 #   gpus:N[:CFG]        python bench.py --gpus N --dist-backend gloo --config CFG (N ranks on this box)
-#   ncu:CFG[:N]         ncu --set full capture of the dominant near launch of CFG (N points)
+#   ncu:CFG[:N[:W]]     ncu --set full capture of the dominant near launch of CFG (N points; W: c5 strip width)
 #   launches:CFG        ncu launch list (gpu__time_duration) of a short bench.py run
 #   c5full              tools/run_c5_full.py (1e7 points, vs the golden)
 #   py:SCRIPT[:ARGS]    python tools/SCRIPT ARGS
+#   export:VAR=VAL      set an environment variable for the tasks after it (unset:VAR clears it)
 # Each profiled command runs once without ncu first and must exit 0.
 TAG=${TAG:-r2}
 mkdir -p gpurun_out
 NCU="ncu --set full --clock-control none --import-source on"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > "gpurun_out/${TAG}_gpu.txt" 2>&1
 for task in "$@"; do
-  IFS=: read -r kind a b <<< "$task"
+  IFS=: read -r kind a b w <<< "$task"
   log="gpurun_out/${TAG}_${kind}${a:+_$a}.log"
   case "$kind" in
     tests)
@@ -36,10 +37,10 @@ for task in "$@"; do
     gpus)
       timeout 1200 python bench.py --gpus "${a:-2}" --dist-backend gloo --config "${b:-c4}" --no-cpu-baseline > "$log" 2>&1 ;;
     ncu)
-      n=${b:+--n $b}
+      n="${b:+--n $b} ${w:+--strip $w}"
       k=near_sym; [ "$a" = c2 ] && k=near_tile
       timeout 600 python tools/profile_step.py "$a" $n --reps 1 > "$log" 2>&1 && \
-        timeout 1200 $NCU -k regex:$k -c 1 -f -o "gpurun_out/${TAG}_${a}_${k}" \
+        timeout 1800 $NCU -k regex:$k -c 1 -f -o "gpurun_out/${TAG}_${a}_${k}" \
           python tools/profile_step.py "$a" $n --reps 1 >> "$log" 2>&1
       echo "ncu rc=$?" >> "$log" ;;
     launches)
@@ -51,7 +52,12 @@ for task in "$@"; do
     c5full)
       timeout 1800 python tools/run_c5_full.py > "$log" 2>&1 ;;
     py)
+      log="gpurun_out/${TAG}_py_${a%.py}${b:+_${b//[,\/ ]/_}}.log"
       timeout 1800 python "tools/$a" ${b//,/ } > "$log" 2>&1 ;;
+    export)
+      export "$a"; continue ;;
+    unset)
+      unset "$a"; continue ;;
     *) echo "unknown task $task" > "$log" ;;
   esac
 done
