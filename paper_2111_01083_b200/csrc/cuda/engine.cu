@@ -361,7 +361,7 @@ int Plan::s2pw_chunks(size_t ns, int modes, int k) const {
   const int mt = k >= 8 ? 1 : 8 / k;
   const int mode_blocks = std::max(1, (modes + mt - 1) / mt);
   long want = (4L * sms_ + mode_blocks - 1) / mode_blocks;
-  const long by_src = static_cast<long>(std::max<size_t>(1, ns / 2048));
+  const long by_src = static_cast<long>(std::max<size_t>(1, ns / 256));  // >= 256 sources per chunk
   want = std::min(want, by_src);
   return static_cast<int>(std::max(1L, std::min(want, 1024L)));
 }
@@ -546,8 +546,11 @@ void Plan::validate(const DevSys& s, const Opts& o, bool far_checks, bool neutra
   double* bm = red_m_.as<double>(kReduceBlocks * kMoments);
   double* bc = red_c_.as<double>(kReduceBlocks * kChecks);
   double* outv = red_out_.as<double>(kMoments + kChecks);
-  launch_reduce(ra, bm, bc, st);
-  launch_sum_blocks(bc, kReduceBlocks, kChecks, outv + kMoments, st);
+  const int rb = reduce_blocks(std::max(ra.ns, ra.nt));
+  launch_reduce(ra, bm, bc, rb, st);
+  launch_sum_blocks(bc, rb, kChecks, outv + kMoments, st);
+  // the block moments of the same sources: source_pass may reuse them (moments_ready)
+  moment_blocks_ = rb;
   cuda_check(cudaGetLastError(), "validate launch");
   const double* h = static_cast<double*>(host_checks_.ensure(64 * sizeof(double)));
   cuda_check(cudaMemcpyAsync(const_cast<double*>(h), outv + kMoments, kChecks * sizeof(double), cudaMemcpyDeviceToHost,
@@ -600,7 +603,7 @@ SpreadArgs Plan::vert_spread_args(const DevSys& s, bool sources) const {
   return a;
 }
 
-void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path) {
+void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path, bool moments_ready) {
   cudaStream_t st = stream_for(o);
   size_t off = 0;
   for (const auto& fp : fams_) {
@@ -670,17 +673,24 @@ void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::
     }
     off += len;
   }
-  // rank-one moments (apply.cpp:68-78, :108-117, :140-146, :179-191)
-  ReduceArgs ra;
-  ra.src = s.src;
-  ra.ns = s.ns;
-  ra.q = kind_of(pz_) == Kind::Scalar ? s.q : nullptr;
-  ra.vec = s.f;
-  ra.nrm = s.nrm;
+  // rank-one moments (apply.cpp:68-78, :108-117, :140-146, :179-191). Right after a
+  // validation of the same system its block moments are already there (the moments used
+  // by the families depend on the sources only; the charge moment only when the kind reads
+  // charges, which is the only case validate's charge sums can differ in).
   double* bm = red_m_.as<double>(kReduceBlocks * kMoments);
-  double* bc = red_c_.as<double>(kReduceBlocks * kChecks);
-  launch_reduce(ra, bm, bc, st);
-  launch_sum_blocks(bm, kReduceBlocks, kMoments, coeff + off, st);
+  int rb = moment_blocks_;
+  if (!(moments_ready && (kind_of(pz_) == Kind::Scalar || s.q == nullptr))) {
+    ReduceArgs ra;
+    ra.src = s.src;
+    ra.ns = s.ns;
+    ra.q = kind_of(pz_) == Kind::Scalar ? s.q : nullptr;
+    ra.vec = s.f;
+    ra.nrm = s.nrm;
+    double* bc = red_c_.as<double>(kReduceBlocks * kChecks);
+    rb = reduce_blocks(s.ns);
+    launch_reduce(ra, bm, bc, rb, st);
+  }
+  launch_sum_blocks(bm, rb, kMoments, coeff + off, st);
   cuda_check(cudaGetLastError(), "source pass launch");
 }
 
@@ -1345,7 +1355,7 @@ bool Plan::total_eager(const DevSys& s, const Opts& o, const DevOut& out, bool f
     const periwave::ApplyPath path = resolve(o, s.ns, s.nt);
     double* coeff = coeff_ws_.as<double>(coeff_size(o, path));
     record(0, st);
-    source_pass(s, o, coeff, path);
+    source_pass(s, o, coeff, path, true);  // validate just reduced these sources
     accelerated = target_pass(s, o, coeff, out, path);
     record(1, st);
     far_timed_ = true;

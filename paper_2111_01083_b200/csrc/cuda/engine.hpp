@@ -174,7 +174,9 @@ class Plan {
   // the path Auto resolves to for the whole (possibly sharded) problem (apply.cpp:424)
   periwave::ApplyPath resolve(const Opts& o, size_t n_src_total, size_t n_tgt_total) const;
   size_t coeff_size(const Opts& o, periwave::ApplyPath path);
-  void source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path);
+  // moments_ready: validate(far_checks) of the same system just ran (its block moments are reused)
+  void source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path,
+                   bool moments_ready = false);
   // returns the accelerated flag (apply.cpp:464-471)
   bool target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out, periwave::ApplyPath path);
   // adds every near image (fused) or one image (single shift)
@@ -219,6 +221,7 @@ class Plan {
   std::vector<std::unique_ptr<Family>> fams_;
   DevBuf s2pw_partial_, coeff_ws_, A_, B_, m0_, near_partial_, flag_, red_m_, red_c_, red_out_;
   PinnedBuf host_checks_;
+  int moment_blocks_ = kReduceBlocks;  // blocks of the last validation reduce (its partials in red_m_)
   DevBuf sym_fx_, sym_rows_, sym_split_ws_, fx_maxhi_;
   PinnedBuf sym_rows_host_;
   // spatially binned copies of the near-field inputs (binning.cu)

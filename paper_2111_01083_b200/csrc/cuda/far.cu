@@ -12,6 +12,8 @@
 // linear in the sources (the multi-GPU allreduce operand).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "pw_engine.cuh"
 
 namespace pwb {
@@ -457,19 +459,25 @@ void launch_s2pw(WeightSet ws, const S2pwArgs& a, cudaStream_t st) {
   }
 }
 
-// Small target counts (c1: 1000 targets = 8 blocks of the kernel above on 148 SMs): one
-// warp per target, lanes stride over the modes, fixed-order xor-shuffle reduction
-// (deterministic). Same per-(target, mode) arithmetic as pw2t_kernel.
-template <int KO, bool HASB, bool GRAD>
+// Small target counts (c1: 1000 targets = 8 blocks of the kernel above on 148 SMs): G warps
+// per target (G = 1: four targets per block; G = 4: one target per block), the group's
+// lanes stride over the modes, fixed-order xor-shuffle reduction inside each warp and a
+// fixed-order sum over the G warps (deterministic). Same per-(target, mode) arithmetic as
+// pw2t_kernel.
+template <int KO, bool HASB, bool GRAD, int G>
 __global__ void __launch_bounds__(kPw2tThreads) pw2t_warp_kernel(const __grid_constant__ Pw2tArgs a) {
-  const size_t l = (static_cast<size_t>(blockIdx.x) * kPw2tThreads + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (l >= a.nt) return;  // whole warps leave together
-  const double2 t = a.tgt[l];
-  double acc[KO * 2 + 4];
+  static_assert(kPw2tThreads % (32 * G) == 0, "whole groups per block");
+  constexpr int NV = KO * 2 + 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t l = static_cast<size_t>(blockIdx.x) * (kPw2tThreads / (32 * G)) + warp / G;
+  const int gl = (warp % G) * 32 + lane;  // lane inside the target's group
+  __shared__ double part[kPw2tThreads / 32][NV];
+  const bool live = l < a.nt;
+  const double2 t = live ? a.tgt[l] : make_double2(0.0, 0.0);
+  double acc[NV];
 #pragma unroll
-  for (int v = 0; v < KO * 2 + 4; ++v) acc[v] = 0.0;
-  for (int r = lane; r < a.modes.count; r += 32) {
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int r = gl; live && r < a.modes.count; r += 32 * G) {
     const int ax = a.modes.axis[r];
     const double wc = ax ? t.x : t.y;
     const double pc = ax ? t.y : t.x;
@@ -510,8 +518,24 @@ __global__ void __launch_bounds__(kPw2tThreads) pw2t_warp_kernel(const __grid_co
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int v = 0; v < KO * 2 + 4; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
-  if (lane != 0) return;
+    for (int v = 0; v < NV; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+  if constexpr (G > 1) {
+    if (lane == 0)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) part[warp][v] = acc[v];
+    __syncthreads();
+    if (warp % G != 0 || lane != 0) return;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double x = part[warp][v];
+#pragma unroll
+      for (int g = 1; g < G; ++g) x += part[warp + g][v];
+      acc[v] = x;
+    }
+  } else if (lane != 0) {
+    return;
+  }
+  if (!live) return;
   double gx_re = acc[KO * 2], gy_re = acc[KO * 2 + 2];
   if (a.m0_lin) {
 #pragma unroll
@@ -563,21 +587,32 @@ void launch_pw2t(const Pw2tArgs& a, cudaStream_t st) {
   int dev = 0, sms = 148;
   cuda_check(cudaGetDevice(&dev), "device");
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  if (grid < static_cast<unsigned>(sms) && a.modes.count >= 64) {  // fewer blocks than SMs: a warp per target
-    const unsigned wgrid = static_cast<unsigned>((a.nt * 32 + kPw2tThreads - 1) / kPw2tThreads);
-    if (a.ko == 1) {
-      if (a.gradient)
-        pw2t_warp_kernel<1, false, true><<<wgrid, kPw2tThreads, 0, st>>>(a);
-      else if (hasb)
-        pw2t_warp_kernel<1, true, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
-      else
-        pw2t_warp_kernel<1, false, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
-    } else {
-      if (hasb)
-        pw2t_warp_kernel<2, true, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
-      else
-        pw2t_warp_kernel<2, false, false><<<wgrid, kPw2tThreads, 0, st>>>(a);
-    }
+  if (grid < static_cast<unsigned>(sms) && a.modes.count >= 64) {  // fewer blocks than SMs: warps per target
+    // a warp per target leaves ~7 warps per SM at c1's 1000 targets, each walking ~40 modes
+    // serially; four warps per target (one target per block) when that still fills the GPU
+    // with at most ~16 blocks per SM
+    const bool wide = a.nt <= static_cast<size_t>(16) * sms && a.modes.count >= 4 * 32 * 4;
+    auto go = [&](auto g) {
+      constexpr int Gv = decltype(g)::value;
+      const unsigned wgrid = static_cast<unsigned>((a.nt * 32 * Gv + kPw2tThreads - 1) / kPw2tThreads);
+      if (a.ko == 1) {
+        if (a.gradient)
+          pw2t_warp_kernel<1, false, true, Gv><<<wgrid, kPw2tThreads, 0, st>>>(a);
+        else if (hasb)
+          pw2t_warp_kernel<1, true, false, Gv><<<wgrid, kPw2tThreads, 0, st>>>(a);
+        else
+          pw2t_warp_kernel<1, false, false, Gv><<<wgrid, kPw2tThreads, 0, st>>>(a);
+      } else {
+        if (hasb)
+          pw2t_warp_kernel<2, true, false, Gv><<<wgrid, kPw2tThreads, 0, st>>>(a);
+        else
+          pw2t_warp_kernel<2, false, false, Gv><<<wgrid, kPw2tThreads, 0, st>>>(a);
+      }
+    };
+    if (wide)
+      go(std::integral_constant<int, 4>{});
+    else
+      go(std::integral_constant<int, 1>{});
     return;
   }
   if (a.ko == 1) {
@@ -595,8 +630,8 @@ void launch_pw2t(const Pw2tArgs& a, cudaStream_t st) {
   }
 }
 
-void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_checks, cudaStream_t st) {
-  reduce_kernel<<<kReduceBlocks, kRedThreads, 0, st>>>(a, block_moments, block_checks);
+void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_checks, int blocks, cudaStream_t st) {
+  reduce_kernel<<<blocks, kRedThreads, 0, st>>>(a, block_moments, block_checks);
   count_launches(1);
 }
 

@@ -611,7 +611,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
         const double shx = a.shx[img], shy = a.shy[img / NXI];
         const bool ident = img == a.id_img;
         int regime = 0;  // per-pair dispatch unless the boxes pin the whole tile pair
-        pwk::ChebFit<kChebDeg> cf;
+        pwk::ChebFit<kChebMax> cf;
         if (a.cull) {
           double lo, hi;
           image_xrange(rb, cbx, shx, shy, a.beta2, lo, hi);
@@ -620,13 +620,15 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
             // regime 3: the tile pair's s = r^2 interval is short enough for one fitted
             // polynomial (block-uniform: every warp fits the same interval identically).
             // x >= 0.5 keeps it clear of the log singularity and of any exact zero.
-            if (a.cheb_tol > 0.0 && lo * 0.9999 > 0.25 &&
-                pwk::cheb_fit_k0(lo * 0.9999, hi * 1.0001, a.beta2, a.inv_beta2, a.cheb_tol, cf))
-              regime = 3;
+            if (a.cheb_tol > 0.0 && lo * 0.9999 > 0.25) {
+              pwk::cheb_fit_k0(lo * 0.9999, hi * 1.0001, a.beta2, a.inv_beta2, a.cheb_tol, cf);
+              if (cf.deg) regime = 3;
+            }
           }
         }
-        auto sweep = [&](auto reg) {
+        auto sweep = [&](auto reg, auto cdeg) {
           constexpr int R = decltype(reg)::value;
+          constexpr int CD = decltype(cdeg)::value;  // regime 3: the fitted degree
           // regime sweeps (no coincidence possible, X_lo > 4): the shifted targets are formed
           // once per image, (t - shift) - s, one subtraction per coordinate and pair; the
           // per-pair dispatch keeps the reference's association (t - s) - shift
@@ -656,7 +658,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
               if constexpr (R == 0) {
                 if (!K::image_value(V, rx, ry, ident, a, flag)) continue;
               } else if constexpr (R == 3) {
-                V[0] = pwk::cheb_eval(cf, rx, ry);
+                V[0] = pwk::cheb_eval<CD>(cf, rx, ry);
               } else {
                 K::template image_fast<R == 2>(V, rx, ry, a);
               }
@@ -667,18 +669,24 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
             for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
           }
         };
+        using I0 = std::integral_constant<int, 0>;
         if constexpr (K::CHEB) {
           if (regime == 3) {
-            sweep(std::integral_constant<int, 3>{});
+            if (cf.deg == 6)
+              sweep(std::integral_constant<int, 3>{}, std::integral_constant<int, 6>{});
+            else if (cf.deg == 9)
+              sweep(std::integral_constant<int, 3>{}, std::integral_constant<int, 9>{});
+            else
+              sweep(std::integral_constant<int, 3>{}, std::integral_constant<int, kChebMax>{});
             continue;
           }
         }
         if (regime == 2)
-          sweep(std::integral_constant<int, 2>{});
+          sweep(std::integral_constant<int, 2>{}, I0{});
         else if (regime == 1 && PWB_SYM_MH_NEAR_SWEEP)
-          sweep(std::integral_constant<int, 1>{});
+          sweep(std::integral_constant<int, 1>{}, I0{});
         else
-          sweep(std::integral_constant<int, 0>{});
+          sweep(std::integral_constant<int, 0>{}, I0{});
       }
       careful = false;
     }

@@ -235,8 +235,14 @@ struct ReduceArgs {
   double d = 1.0, xi = 0.0, eta = 1.0;
 };
 constexpr int kReduceBlocks = 296;
+// blocks of the validation / moment reduction for n points: 296 (2 per SM) from ~300K points
+// on, fewer for small problems (c1: 1) so the block partials' final sum stays short
+inline int reduce_blocks(size_t n) {
+  const size_t b = (n + 1023) / 1024;
+  return static_cast<int>(b < 1 ? 1 : (b > static_cast<size_t>(kReduceBlocks) ? kReduceBlocks : b));
+}
 // writes per-block partials: moments [blocks][kMoments], checks [blocks][kChecks]
-void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_checks, cudaStream_t st);
+void launch_reduce(const ReduceArgs& a, double* block_moments, double* block_checks, int blocks, cudaStream_t st);
 void launch_sum_blocks(const double* block_vals, int blocks, int n, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- NUFFT lines (nufft.cu)
