@@ -471,22 +471,26 @@ class FieldResult:
 
 
 def _kind(pz: Periodizer) -> str:
-    inf = pz.info()
-    if inf["multipole_order"] >= 1:
-        return "multipole"
-    if inf["pde"] in (Pde.Stokes, Pde.ModStokes):
-        return "velocity"
-    return "scalar"
+    k = getattr(pz, "_kind_cache", None)  # the tables are immutable: one info() per periodizer
+    if k is None:
+        inf = pz.info()
+        k = ("multipole" if inf["multipole_order"] >= 1 else
+             "velocity" if inf["pde"] in (Pde.Stokes, Pde.ModStokes) else "scalar")
+        pz._kind_cache = k
+    return k
 
 
-def _alloc(like_device: bool, shape, ref=None):
+def _alloc(like_device: bool, shape, ref=None, zero=True):
     if like_device:
         import torch
-        return torch.zeros(shape, dtype=torch.float64, device=ref.device if ref is not None else "cuda")
+        dev = ref.device if ref is not None else "cuda"
+        # overwriting entry points fill every element: no zero-fill kernel
+        return (torch.zeros if zero else torch.empty)(shape, dtype=torch.float64, device=dev)
     return np.zeros(shape)
 
 
-def _field_for(pz: Periodizer, opt: ApplyOptions, nt: int, device: bool, ref, out: Optional[FieldResult]):
+def _field_for(pz: Periodizer, opt: ApplyOptions, nt: int, device: bool, ref, out: Optional[FieldResult],
+               zero: bool = True):
     k = _kind(pz)
     res = out if out is not None else FieldResult()
     f = _Field()
@@ -495,7 +499,7 @@ def _field_for(pz: Periodizer, opt: ApplyOptions, nt: int, device: bool, ref, ou
     def ensure(name, shape):
         cur = getattr(res, name)
         if cur is None:
-            cur = _alloc(device, shape, ref)
+            cur = _alloc(device, shape, ref, zero)
             setattr(res, name, cur)
         p, _ = _ptr_mem(cur, nt, int(np.prod(shape[1:])) if len(shape) > 1 else 1, name)
         return p
@@ -513,10 +517,10 @@ def _field_for(pz: Periodizer, opt: ApplyOptions, nt: int, device: bool, ref, ou
     return res, f
 
 
-def _apply(fn, pz: Periodizer, sys: ParticleSystem, opt: Optional[ApplyOptions], out=None, extra=()):
+def _apply(fn, pz: Periodizer, sys: ParticleSystem, opt: Optional[ApplyOptions], out=None, extra=(), zero=True):
     opt = opt or ApplyOptions()
     s, mem = sys._c()
-    res, f = _field_for(pz, opt, s.n_tgt, mem == MEM_DEVICE, sys.targets if mem == MEM_DEVICE else None, out)
+    res, f = _field_for(pz, opt, s.n_tgt, mem == MEM_DEVICE, sys.targets if mem == MEM_DEVICE else None, out, zero)
     o = opt._c()
     _check(fn(pz.handle, ctypes.byref(s), *extra, ctypes.byref(o), ctypes.byref(f)))
     res.accelerated = bool(f.accelerated)
@@ -525,12 +529,12 @@ def _apply(fn, pz: Periodizer, sys: ParticleSystem, opt: Optional[ApplyOptions],
 
 def total_field(pz: Periodizer, sys: ParticleSystem, opt: Optional[ApplyOptions] = None) -> FieldResult:
     """Far apply + fused near images (reference apply.cpp:548-556)."""
-    return _apply(lib().pwb_total_field, pz, sys, opt)
+    return _apply(lib().pwb_total_field, pz, sys, opt, zero=False)
 
 
 def apply_far(pz: Periodizer, sys: ParticleSystem, opt: Optional[ApplyOptions] = None) -> FieldResult:
     """Low-rank plane-wave far field (reference apply.cpp:417-479)."""
-    return _apply(lib().pwb_apply_far, pz, sys, opt)
+    return _apply(lib().pwb_apply_far, pz, sys, opt, zero=False)
 
 
 def accumulate(pz: Periodizer, sys: ParticleSystem, shift, identity_shift: bool, opt: Optional[ApplyOptions],
@@ -628,7 +632,7 @@ def far_target_pass(pz: Periodizer, sys: ParticleSystem, coeff, opt: Optional[Ap
     s, mem = sys._c()
     if mem != MEM_DEVICE:
         raise ValueError("far_target_pass takes device tensors")
-    res, f = _field_for(pz, opt, s.n_tgt, True, sys.targets, out)
+    res, f = _field_for(pz, opt, s.n_tgt, True, sys.targets, out, zero=False)
     o = opt._c()
     _check(lib().pwb_far_target_pass(pz.handle, ctypes.byref(s), ctypes.byref(o), n_src_total, n_tgt_total,
                                      coeff.data_ptr(), ctypes.byref(f)))

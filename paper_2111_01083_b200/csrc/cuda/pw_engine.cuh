@@ -235,10 +235,10 @@ struct ReduceArgs {
   double d = 1.0, xi = 0.0, eta = 1.0;
 };
 constexpr int kReduceBlocks = 296;
-// blocks of the validation / moment reduction for n points: 296 (2 per SM) from ~300K points
-// on, fewer for small problems (c1: 1) so the block partials' final sum stays short
+// blocks of the validation / moment reduction for n points: 296 (2 per SM) from ~76K points
+// on, one per 256 points below (c1: 4), so the block partials' final sum stays short
 inline int reduce_blocks(size_t n) {
-  const size_t b = (n + 1023) / 1024;
+  const size_t b = (n + 255) / 256;
   return static_cast<int>(b < 1 ? 1 : (b > static_cast<size_t>(kReduceBlocks) ? kReduceBlocks : b));
 }
 // writes per-block partials: moments [blocks][kMoments], checks [blocks][kChecks]
