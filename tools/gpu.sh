@@ -38,7 +38,7 @@ for task in "$@"; do
       timeout 1200 python bench.py --gpus "${a:-2}" --dist-backend gloo --config "${b:-c4}" --no-cpu-baseline > "$log" 2>&1 ;;
     ncu)
       n="${b:+--n $b} ${w:+--strip $w}"
-      k=near_sym; [ "$a" = c2 ] && k=near_tile
+      k=near_sym; { [ "$a" = c2 ] || [ "$a" = c1 ]; } && k=near_tile
       timeout 600 python tools/profile_step.py "$a" $n --reps 1 > "$log" 2>&1 && \
         timeout 1800 $NCU -k regex:$k -c 1 -f -o "gpurun_out/${TAG}_${a}_${k}" \
           python tools/profile_step.py "$a" $n --reps 1 >> "$log" 2>&1
