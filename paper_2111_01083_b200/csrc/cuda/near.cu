@@ -85,6 +85,32 @@ struct Laplace {  // -log|r| / 2pi  (kernels.cpp:102-103)
       acc[0] = fma(w[0], LP, acc[0]);
       return;
     }
+    // A self pair (targets == sources) or a duplicate point: the identity image's exact zero
+    // is skipped (apply.cpp:536-539) and the other images' product is normally fine -- one
+    // log of it. (Without this shortcut every self pair ran the per-image loop below, and the
+    // one warp of a block holding the block's self pairs ran it once per source: c1's near
+    // tile went 37 -> ~5 us.) Any other exact zero flags the coincidence.
+    double Q = 1.0;
+    bool other_zero = false;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n)
+#pragma unroll
+      for (int m = 0; m < NXI; ++m) {
+        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = row_dy<NXI, NROW>(dy, a, n);
+        if (rx == 0.0 && ry == 0.0) {
+          if (n * NXI + m != a.id_img) other_zero = true;
+          continue;
+        }
+        Q *= fma(rx, rx, ry * ry);
+      }
+    if (other_zero) flag = 1;
+    int bad2 = 0;
+    const double LQ = pwk::log_pos_k<LOWP>(Q, C, bad2);
+    if (!bad2 && !other_zero) {
+      acc[0] = fma(w[0], LQ, acc[0]);
+      return;
+    }
     double L = 0.0;
 #pragma unroll 1
     for (int n = 0; n < NROW; ++n)

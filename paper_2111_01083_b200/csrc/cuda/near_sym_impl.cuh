@@ -80,6 +80,9 @@ namespace sym {
 #ifndef PWB_SYM_LAPLACE_REPL
 #define PWB_SYM_LAPLACE_REPL 8  // log-table replicas of the Laplace tile (8: conflict-free LDS.128)
 #endif
+#ifndef PWB_SYM_CLOG_REPL
+#define PWB_SYM_CLOG_REPL 4  // replicas of the coarse (256-entry) table: 4 x 4 KB keeps 7 blocks/SM
+#endif
 #ifndef PWB_SYM_STOKES_TPT
 #define PWB_SYM_STOKES_TPT 2  // targets per thread of the Stokeslet tile
 #endif
@@ -146,7 +149,7 @@ struct SymLaplace {
   // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
   // blocks per SM fit
-  static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = CLOG ? 4 : PWB_SYM_LAPLACE_REPL,
+  static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = CLOG ? PWB_SYM_CLOG_REPL : PWB_SYM_LAPLACE_REPL,
                        LOG_BITS = CLOG ? 8 : pwk::kLogTabBits;  // 256 x 4 x 16 B = 16 KB, 7 blocks still fit
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,

@@ -15,6 +15,9 @@
 #   c5full              tools/run_c5_full.py (1e7 points, vs the golden)
 #   py:SCRIPT[:ARGS]    python tools/SCRIPT ARGS
 #   export:VAR=VAL      set an environment variable for the tasks after it (unset:VAR clears it)
+#   ab:TU:FLAGS:CFG     rebuild translation unit csrc/cuda/TU.cu with EXTRA_NVFLAGS=FLAGS (comma-separated
+#                       -D... flags; "default" = none), relink, time one warm CFG step (profile_step);
+#                       the library stays in that state until the next ab task
 # Each profiled command runs once without ncu first and must exit 0.
 TAG=${TAG:-r2}
 mkdir -p gpurun_out
@@ -54,6 +57,13 @@ for task in "$@"; do
     py)
       log="gpurun_out/${TAG}_py_${a%.py}${b:+_${b//[,\/ ]/_}}.log"
       timeout 1800 python "tools/$a" ${b//,/ } > "$log" 2>&1 ;;
+    ab)
+      flags=""; [ "$b" != default ] && flags="${b//,/ }"
+      log="gpurun_out/${TAG}_ab_${a}_${b//[,=\/ ]/_}.log"
+      touch "paper_2111_01083_b200/csrc/cuda/$a.cu"
+      make -C paper_2111_01083_b200 -j8 EXTRA_NVFLAGS="$flags" > "$log" 2>&1 && \
+        timeout 900 python tools/profile_step.py "${w:-c4}" --reps 3 >> "$log" 2>&1
+      echo "ab rc=$?" >> "$log" ;;
     export)
       export "$a"; continue ;;
     unset)
