@@ -96,7 +96,7 @@ namespace sym {
 #define PWB_SYM_KEEP_SMEM 0  // 1: the fast path's pre-tile row sums live in shared memory (frees registers)
 #endif
 #ifndef PWB_SYM_LAPLACE_MINB
-#define PWB_SYM_LAPLACE_MINB 7  // 7 x 4 warps/SM at 72 registers (128-point column tiles leave room in shared memory): c4 667 -> 653 ms vs 6
+#define PWB_SYM_LAPLACE_MINB 8  // 8 x 4 warps/SM at 64 registers (the cold careful path spills 32 B): c4 near 637.3 / 639.1 -> 632.9 / 632.7 ms vs 7 (r2i, r2j); 7 beat 6 (667 -> 653)
 #endif
 constexpr int kT = 128;  // threads per block
 constexpr int kSymMhUnrollM = PWB_SYM_MH_UNROLL_M;
