@@ -636,3 +636,35 @@ def test_symmetric_tile_tiers(pw, gpu, pde, strength):
     low_sym = getattr(pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, **kw)), key)
     assert rel_l2(full_sym, full_one) <= 1e-13
     assert rel_l2(low_sym, full_one) <= 1e-12
+
+
+@pytest.mark.parametrize("sym", [True, False])
+def test_screening_cutoff_with_cancelling_charges(pw, gpu, ref, sym):
+    """The screened tiles skip pairs with beta r >= x_c, x_c from a bound relative to
+    max |q| (engine.cu screen_cutoff). Adversarial case: every source is half of a tight
+    dipole (q, -q at 1e-3), so the field is ~1e-3 of a monopole field and the bound, taken
+    at face value, would be 1e3 times too loose -- but the skipped tail cancels the same way
+    (the dipole's K0 difference decays like K1), so the result still meets 10 eps against
+    the reference, which sums every pair. c5's cell and beta; symmetric and one-sided tiles."""
+    rng = np.random.default_rng(11)
+    m = 20000
+    d, xi, eta = 100.0, 0.0, 1.0
+    u = rng.uniform(-0.499, 0.499, (m, 2))
+    a = np.column_stack([u[:, 0] * d, u[:, 1] * eta])
+    ang = rng.uniform(0, 2 * np.pi, m)
+    b = a + 1e-3 * np.column_stack([np.cos(ang), np.sin(ang)])
+    src = np.ascontiguousarray(np.concatenate([a, b]))
+    qa = rng.standard_normal(m)
+    q = np.ascontiguousarray(np.concatenate([qa, -qa]))
+    eps = 1e-8
+    cellt = (d, xi, eta, 2)
+    pz = pw.make_periodizer(pw.Pde.ModHelmholtz, 1.0, _cell(pw, cellt), eps)
+    tgt = src if sym else np.ascontiguousarray(src.copy())
+    got = pw.total_field(pz, pw.ParticleSystem(sources=src, targets=tgt, charges=q),
+                         pw.ApplyOptions(path=pw.ApplyPath.Direct)).scalar
+    idx = rng.choice(2 * m, 96, replace=False)
+    R = ref.make_periodizer(1, 1.0, cellt, eps)
+    want = R.apply(0, src, np.ascontiguousarray(src[idx]), charges=q, path=1, threads=8)["scalar"]
+    err = rel_l2(got[idx], want)
+    print("dipole field rel l2", err, "field / monopole scale", np.linalg.norm(want) / np.linalg.norm(qa))
+    assert err <= 10 * eps
