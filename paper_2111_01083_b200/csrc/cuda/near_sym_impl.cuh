@@ -83,6 +83,9 @@ namespace sym {
 #ifndef PWB_SYM_CLOG_REPL
 #define PWB_SYM_CLOG_REPL 4  // replicas of the coarse (256-entry) table: 4 x 4 KB keeps 7 blocks/SM
 #endif
+#ifndef PWB_SYM_CLOG_TAB
+#define PWB_SYM_CLOG_TAB 8  // coarse table code (pw_math.cuh tab_bits / log_f_deg): 8 = 256 x degree 2
+#endif
 #ifndef PWB_SYM_STOKES_TPT
 #define PWB_SYM_STOKES_TPT 2  // targets per thread of the Stokeslet tile
 #endif
@@ -150,7 +153,7 @@ struct SymLaplace {
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
   // blocks per SM fit
   static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = CLOG ? PWB_SYM_CLOG_REPL : PWB_SYM_LAPLACE_REPL,
-                       LOG_BITS = CLOG ? 8 : pwk::kLogTabBits;  // 256 x 4 x 16 B = 16 KB, 7 blocks still fit
+                       LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;  // 256 x 4 x 16 B = 16 KB
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -311,7 +314,7 @@ struct SymStokes {
                        TPT = PWB_SYM_STOKES_TPT, CPT = PWB_SYM_STOKES_CPT < PWB_SYM_STOKES_TPT ? PWB_SYM_STOKES_CPT
                                                                                                 : PWB_SYM_STOKES_TPT,
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
-                       LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? 8 : pwk::kLogTabBits;
+                       LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -522,9 +525,9 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   // log constants in registers; the reduced tier's log table in shared memory
   constexpr size_t kTileSmem = sizeof(double) * (static_cast<size_t>(CT) * (2 + K::NW) + kWarps * K::NACC * CT);
   constexpr int kRepl = K::LOG_REPL, kBits = K::LOG_BITS;
-  constexpr size_t kTabSmem = sizeof(double2) * (size_t{1} << kBits) * kRepl;
+  constexpr size_t kTabSmem = sizeof(double2) * (size_t{1} << pwk::tab_bits(kBits)) * kRepl;
   constexpr bool kTab = K::FAST && K::LOWP && PWB_SYM_LOG_TABLE && kTileSmem + kTabSmem <= 48 * 1024;
-  __shared__ double2 s_lt[kTab ? (1 << kBits) * kRepl : 1];
+  __shared__ double2 s_lt[kTab ? (1 << pwk::tab_bits(kBits)) * kRepl : 1];
   using LKT = std::conditional_t<kTab, pwk::LogT<kRepl, kBits>, pwk::LogK<K::LOWP>>;
   LKT LK;
   if constexpr (kTab) {
