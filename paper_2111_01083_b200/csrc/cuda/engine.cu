@@ -657,8 +657,11 @@ void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::
     }
     const size_t len = static_cast<size_t>(f.count) * k * 2;
     if (f.count > 0) {
-      const int chunks = s.ns == 0 ? 1 : s2pw_chunks(s.ns, f.count, k);
+      // small problems: one chunk, one mode per block, the kernel writes the raw sums
+      const bool narrow = s.ns <= kS2pwNarrowSources;
+      const int chunks = (s.ns == 0 || narrow) ? 1 : s2pw_chunks(s.ns, f.count, k);
       S2pwArgs a;
+      a.narrow = narrow ? 1 : 0;
       a.modes = f.table();
       a.src = s.src;
       a.q = s.q;
@@ -667,9 +670,14 @@ void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::
       a.ns = s.ns;
       a.chunks = chunks;
       a.per_chunk = (s.ns + chunks - 1) / chunks;
-      a.partial = s2pw_partial_.as<double>(static_cast<size_t>(chunks) * len);
-      launch_s2pw(f.ws, a, st);
-      launch_chunk_sum(a.partial, chunks, len, coeff + off, st);
+      if (chunks == 1) {
+        a.partial = coeff + off;
+        launch_s2pw(f.ws, a, st);
+      } else {
+        a.partial = s2pw_partial_.as<double>(static_cast<size_t>(chunks) * len);
+        launch_s2pw(f.ws, a, st);
+        launch_chunk_sum(a.partial, chunks, len, coeff + off, st);
+      }
     }
     off += len;
   }

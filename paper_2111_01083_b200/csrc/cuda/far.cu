@@ -159,8 +159,12 @@ template <WeightSet WS>
 void s2pw_dispatch(const S2pwArgs& a, cudaStream_t st) {
   constexpr int K = Weights<WS>::K;
   constexpr int MT = K >= 8 ? 1 : 8 / K;
-  dim3 grid((a.modes.count + MT - 1) / MT, a.chunks);
-  s2pw_kernel<WS, MT><<<grid, kS2pwThreads, 0, st>>>(a);
+  if (a.narrow) {  // c1: 1344 + 32 blocks of 128 threads, 8 sources per thread, no chunk sum
+    s2pw_kernel<WS, 1><<<dim3(a.modes.count, a.chunks), kS2pwThreads, 0, st>>>(a);
+  } else {
+    dim3 grid((a.modes.count + MT - 1) / MT, a.chunks);
+    s2pw_kernel<WS, MT><<<grid, kS2pwThreads, 0, st>>>(a);
+  }
   count_launches(1);
 }
 
@@ -587,7 +591,7 @@ void launch_pw2t(const Pw2tArgs& a, cudaStream_t st) {
   int dev = 0, sms = 148;
   cuda_check(cudaGetDevice(&dev), "device");
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  if (grid < static_cast<unsigned>(sms) && a.modes.count >= 64) {  // fewer blocks than SMs: warps per target
+  if (grid < static_cast<unsigned>(sms) && a.modes.count >= 16) {  // fewer blocks than SMs: warps per target
     // a warp per target leaves ~7 warps per SM at c1's 1000 targets, each walking ~40 modes
     // serially; four warps per target (one target per block) when that still fills the GPU
     // with at most ~16 blocks per SM

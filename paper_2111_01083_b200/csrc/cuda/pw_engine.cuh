@@ -174,8 +174,11 @@ struct S2pwArgs {
   size_t ns = 0;
   size_t per_chunk = 0;
   int chunks = 1;
-  double* partial = nullptr;  // [chunk][mode][K][2]
+  double* partial = nullptr;  // [chunk][mode][K][2] (chunks == 1: the raw sums themselves)
+  int narrow = 0;             // 1: one mode per block (small problems: more blocks, shorter chains)
 };
+// small source counts take one chunk and one mode per block (s2pw_kernel<WS, 1>)
+constexpr size_t kS2pwNarrowSources = 4096;
 void launch_s2pw(WeightSet ws, const S2pwArgs& a, cudaStream_t st);
 // sums partial over chunks (fixed order) into raw[mode][K][2]
 void launch_chunk_sum(const double* partial, int chunks, size_t per_chunk_len, double* raw, cudaStream_t st);
