@@ -176,6 +176,11 @@ Plan::~Plan() {
   for (auto& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (capture_stream_) cudaStreamDestroy(capture_stream_);
+  for (auto& side : side_)
+    if (side) cudaStreamDestroy(side);
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
+  for (auto& e : side_done_)
+    if (e) cudaEventDestroy(e);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
@@ -603,7 +608,8 @@ SpreadArgs Plan::vert_spread_args(const DevSys& s, bool sources) const {
   return a;
 }
 
-void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path, bool moments_ready) {
+void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path, bool moments_ready,
+                       cudaEvent_t moments_after) {
   cudaStream_t st = stream_for(o);
   size_t off = 0;
   for (const auto& fp : fams_) {
@@ -687,6 +693,8 @@ void Plan::source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::
   // charges, which is the only case validate's charge sums can differ in).
   double* bm = red_m_.as<double>(kReduceBlocks * kMoments);
   int rb = moment_blocks_;
+  // a validation branch owns red_m_ / red_c_ until its event (reused or overwritten below)
+  if (moments_after) cuda_check(cudaStreamWaitEvent(st, moments_after, 0), "moments wait");
   if (!(moments_ready && (kind_of(pz_) == Kind::Scalar || s.q == nullptr))) {
     ReduceArgs ra;
     ra.src = s.src;
@@ -1164,7 +1172,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   // one-sided tile with source splits is faster there)
   const bool symmetric = !single && s.tgt == s.src && s.nt == s.ns && s.nt >= 32768 && near_sym_supported(nk) &&
                          std::getenv("PWB_NO_SYMMETRIC") == nullptr;
-  record(2, st);
+  record(2, branch_ ? side_[1] : st);  // on the branch the tile starts at the fork
   // screened kernels branch on beta*r per pair: bin so the branch is warp-uniform
   const bool screened = near_screened(nk, a);
   if (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)
@@ -1182,6 +1190,10 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   }
   if (!done) {
     double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
+    if (branch_) {  // a split tile runs on the near branch, its reduction here after the far pass
+      a.tile_stream = side_[1];
+      a.tile_done = side_done_[1];
+    }
     launch_near(nk, a, st, ws, sms_);
   }
   record(3, st);
@@ -1323,6 +1335,7 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
     e.accelerated = total_eager(s, oc, gout, far, near_images);
   } catch (...) {
     defer_ = false;
+    branch_ = false;
     cudaStreamEndCapture(capture_stream_, &graph);
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
@@ -1354,16 +1367,37 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
   return launch(graphs_.back());
 }
 
+void Plan::ensure_side() {
+  if (side_[0]) return;
+  for (auto& side : side_) cuda_check(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "event");
+  for (auto& e : side_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+}
+
 bool Plan::total_eager(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
   bool accelerated = false;
   cudaStream_t st = stream_for(o);
   far_timed_ = near_timed_ = false;
+  // Capturing a small call (graph replay): the validation reductions and the near tile do not
+  // feed the far pass (the checks are deferred to after the replay), so they become parallel
+  // branches forked at the start: validation joins before the moment sum that reuses its
+  // partials, the tile before the reduction of its split partials into the outputs.
+  branch_ = defer_ && far && near_images;
+  if (branch_) {
+    ensure_side();
+    cuda_check(cudaEventRecord(fork_ev_, st), "fork");
+    for (auto& side : side_) cuda_check(cudaStreamWaitEvent(side, fork_ev_, 0), "fork wait");
+  }
   if (far) {
-    validate(s, o, true);
+    Opts ov = o;
+    if (branch_) ov.stream = side_[0];
+    validate(s, ov, true);
+    if (branch_) cuda_check(cudaEventRecord(side_done_[0], side_[0]), "validation join");
     const periwave::ApplyPath path = resolve(o, s.ns, s.nt);
     double* coeff = coeff_ws_.as<double>(coeff_size(o, path));
     record(0, st);
-    source_pass(s, o, coeff, path, true);  // validate just reduced these sources
+    // validate just reduced these sources (on the branch: the moment sum waits for it)
+    source_pass(s, o, coeff, path, true, branch_ ? side_done_[0] : nullptr);
     accelerated = target_pass(s, o, coeff, out, path);
     record(1, st);
     far_timed_ = true;
@@ -1371,6 +1405,10 @@ bool Plan::total_eager(const DevSys& s, const Opts& o, const DevOut& out, bool f
   if (near_images) {
     if (!far) validate(s, o, false);
     near(s, o, out, false, 0.0, 0.0, false);
+  }
+  if (branch_) {  // every branch rejoins the origin stream before the capture ends
+    cuda_check(cudaStreamWaitEvent(st, side_done_[0], 0), "validation join wait");
+    branch_ = false;
   }
   return accelerated;
 }

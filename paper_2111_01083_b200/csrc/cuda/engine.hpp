@@ -175,8 +175,9 @@ class Plan {
   periwave::ApplyPath resolve(const Opts& o, size_t n_src_total, size_t n_tgt_total) const;
   size_t coeff_size(const Opts& o, periwave::ApplyPath path);
   // moments_ready: validate(far_checks) of the same system just ran (its block moments are reused)
+  // moments_after: an event (the validation branch of a captured call) the moment sum waits for
   void source_pass(const DevSys& s, const Opts& o, double* coeff, periwave::ApplyPath path,
-                   bool moments_ready = false);
+                   bool moments_ready = false, cudaEvent_t moments_after = nullptr);
   // returns the accelerated flag (apply.cpp:464-471)
   bool target_pass(const DevSys& s, const Opts& o, const double* coeff, const DevOut& out, periwave::ApplyPath path);
   // adds every near image (fused) or one image (single shift)
@@ -261,6 +262,11 @@ class Plan {
   std::vector<GraphKey> seen_;
   unsigned long graph_epoch_ = 0;
   cudaStream_t capture_stream_ = nullptr;
+  // parallel branches of a captured call: [0] validation, [1] the near tile
+  cudaStream_t side_[2] = {nullptr, nullptr};
+  cudaEvent_t fork_ev_ = nullptr, side_done_[2] = {nullptr, nullptr};
+  bool branch_ = false;  // total_eager is capturing with branches (near() puts its tile on side_[1])
+  void ensure_side();
   DevBuf graph_out_;  // the graph writes here; each replay copies into the caller's arrays
 
   VertAccel va_;

@@ -673,8 +673,15 @@ void launch_shape(const NearArgs& a0, cudaStream_t st, double* partial_ws, int s
   a.src_per_split = ((a.src_per_split + 7) / 8) * 8;
   a.partial = partial_ws;
   dim3 grid(bx, splits);
-  near_tile_kernel<KER, NXI, NROW, TPT><<<grid, kThreads, 0, st>>>(a);
+  // with splits the tile only writes partials: it may run on the branch stream, joined here
+  cudaStream_t ts = (a.tile_stream && splits > 1) ? static_cast<cudaStream_t>(a.tile_stream) : st;
+  near_tile_kernel<KER, NXI, NROW, TPT><<<grid, kThreads, 0, ts>>>(a);
   count_launches(1);
+  if (a.tile_stream) {  // always join the branch (it may have been forked with nothing on it)
+    auto done = static_cast<cudaEvent_t>(a.tile_done);
+    cuda_check(cudaEventRecord(done, static_cast<cudaStream_t>(a.tile_stream)), "tile join");
+    cuda_check(cudaStreamWaitEvent(st, done, 0), "tile join wait");
+  }
   if (splits > 1) {
     const size_t n = a.nt * KER::NOUT;
     if (n < 65536 && splits >= 8)

@@ -88,6 +88,10 @@ struct NearArgs {
   int coarse_log = 0;            // symmetric Laplace / Stokeslet tiles: 256-entry table log (eps >= 1e-10)
   double cheb_tol = 0.0;         // screened symmetric tile: per-tile-pair Chebyshev K0 fit (0: off)
   double inv_beta2 = 0.0;
+  // host side only: a split one-sided tile may run on its own stream (a parallel branch of a
+  // captured small call, engine.cu total_eager); the partials' reduction waits for tile_done
+  void* tile_stream = nullptr;
+  void* tile_done = nullptr;
 };
 
 // ---------------------------------------------------------------- spatial binning (binning.cu)
