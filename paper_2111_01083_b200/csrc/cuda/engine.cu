@@ -1164,7 +1164,8 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   NearArgs a;
   const NearKind nk = near_args(s, o, out, single, shx, shy, identity, a);
   int* flag = flag_.as<int>(1);
-  cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
+  // on the near branch of a captured call the tile starts at the fork: clear its flag there
+  cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), branch_ ? side_[1] : st), "memset flag");
   a.flag = flag;
   const size_t nout = near_outputs(nk);
   // targets == sources (same array): every unordered pair once (near_sym.cu)
