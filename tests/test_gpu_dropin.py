@@ -48,8 +48,10 @@ def test_dropin_total_field_is_the_capi_fast_path(gpu, tmp_path, name):
     line, a, b = _run(name, tmp_path)
     if name == "c3":  # Direct far field: the whole result is deterministic
         assert np.array_equal(a, b)
-    else:  # c4's Auto path is the type-3 NUFFT (spreading sums in atomic order): ~1 ulp
-        assert rel_l2(a, b, gauge=True) <= 1e-14
+    else:  # c4's Auto path is the type-3 NUFFT (spreading sums in atomic order): the Poisson
+        # gauge constant moves (O(1)), the rest agrees to ~1e-14; the one-sided tile would
+        # differ from the symmetric one by ~1e-12 (test_symmetric_targets_equal_sources)
+        assert rel_l2(a, b, gauge=True) <= 1e-13
     # same tile, same staging: the reference-shaped call costs what the C-ABI call costs
     assert line["dropin_median_ms"] <= 1.05 * line["capi_median_ms"] + 2.0, line
     print(json.dumps({"config": name, **line}))
