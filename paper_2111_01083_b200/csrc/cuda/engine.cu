@@ -1177,7 +1177,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   // screened kernels branch on beta*r per pair: bin so the branch is warp-uniform
   const bool screened = near_screened(nk, a);
   if (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)
-    bin_inputs(s, a, st);
+    bin_inputs(s, a, branch_ ? side_[1] : st);  // the tile's stream (captured calls never bin today)
   bool done = false;
   if (symmetric) {
     const size_t nb = near_sym_tiles(s.nt);
