@@ -63,3 +63,13 @@ def test_dropin_small_system_reuses_the_plan(gpu, tmp_path):
     line, a, b = _run("c1", tmp_path, reps=20)
     assert np.array_equal(a, b)
     assert line["dropin_median_ms"] < 0.25 * line["dropin_first_ms"], line
+
+
+def test_plan_cache_under_eviction(gpu):
+    """12 distinct periodizers round-robin through the drop-in API's 8-entry plan cache
+    (evictions every round, equal copies hitting the same entry): every result equals the
+    first result of the same periodizer bitwise."""
+    r = subprocess.run([BIN, "--cache-check"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["mismatches"] == 0 and line["calls"] == 36
