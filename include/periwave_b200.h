@@ -181,7 +181,12 @@ typedef struct {
  * apply_far (proj/src/apply.cpp:417-479, apply.hpp:52-53): overwritten.
  * accumulate = FreeSpaceEvaluator::accumulate (proj/src/apply.cpp:481-546,
  *   apply.hpp:42-44): ADDS one image's direct sum into *out.
- * near_field: ADDS every near_translations image (one fused launch). */
+ * near_field: ADDS every near_translations image (one fused launch).
+ * Host systems (PWB_MEM_HOST) whose targets hold the same bytes as their sources are staged
+ * as one device array (the symmetric near tile). Small total_field calls (one-sided near
+ * tile, N_S N_T <= ~4.2e6) replay a CUDA graph captured on their second repetition with the
+ * same pointers and sizes (PWB_NO_GRAPH=1 disables it); errors are still returned, but the
+ * device output arrays of such a failed call are unspecified. */
 int pwb_total_field(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, pwb_field* out);
 int pwb_apply_far(const pwb_periodizer* pz, const pwb_system* sys, const pwb_options* opt, pwb_field* out);
 int pwb_accumulate(const pwb_periodizer* pz, const pwb_system* sys, double shift_x, double shift_y,
