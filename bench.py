@@ -529,7 +529,14 @@ def main():
     import ctypes
 
     peak = ctypes.c_double(0.0)
-    pw.lib().pwb_fp64_peak_probe(-1, ctypes.byref(peak))
+    if sharded:  # one rank at a time: ranks sharing a GPU must not halve each other's probe
+        for r in range(ws):
+            dist.barrier()
+            if r == rank:
+                pw.lib().pwb_fp64_peak_probe(-1, ctypes.byref(peak))
+        dist.barrier()
+    else:
+        pw.lib().pwb_fp64_peak_probe(-1, ctypes.byref(peak))
     nimg = len(pw.near_translations(cell))
     sym_tile = symmetric and (sharded or ns >= 32768)
     roof = roofline(args.config, ns, nt, sym_tile, ws, t_near, peak.value, nimg)
