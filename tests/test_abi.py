@@ -1,7 +1,6 @@
 """The C-ABI boundary: the library loads on a CPU-only box, exports every symbol
 include/periwave_b200.h declares, and its host-only entry points behave like the
 reference's (no GPU compute here)."""
-import ctypes
 import os
 import re
 
