@@ -1257,6 +1257,7 @@ void Plan::drop_graphs() {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   graphs_.clear();
   seen_.clear();
+  no_graph_.clear();
 }
 
 bool Plan::total(const DevSys& s, const Opts& o, const DevOut& out, bool far, bool near_images) {
@@ -1310,6 +1311,8 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
   };
   for (const auto& e : graphs_)
     if (e.key == k) return launch(e);
+  if (std::find(no_graph_.begin(), no_graph_.end(), k) != no_graph_.end())
+    return total_eager(s, o, out, far, near_images);
   if (std::find(seen_.begin(), seen_.end(), k) == seen_.end()) {
     // first sighting: run eagerly (sizes every workspace and one-time setup), remember it
     own_outputs();  // size the output block now, so the capture does not move a buffer
@@ -1332,28 +1335,45 @@ bool Plan::total_graphed(const DevSys& s, const Opts& o, const DevOut& out, bool
   cudaGraph_t graph = nullptr;
   own_outputs();
   const DevOut gout{own[0], own[1], own[2], own[3], own[4]};
-  try {
-    e.accelerated = total_eager(s, oc, gout, far, near_images);
-  } catch (...) {
+  auto abandon = [&] {  // end the capture and forget it (the CUDA error state is cleared)
     defer_ = false;
     branch_ = false;
     cudaStreamEndCapture(capture_stream_, &graph);
     if (graph) cudaGraphDestroy(graph);
+    graph = nullptr;
     cudaGetLastError();
+    count_launches(-(launch_count() - l0));
     pending_.clear();
+  };
+  try {
+    e.accelerated = total_eager(s, oc, gout, far, near_images);
+  } catch (const CudaFailure&) {
+    // the capture itself failed (an operation the driver cannot capture): this call shape
+    // runs eagerly from now on
+    abandon();
+    no_graph_.push_back(k);
+    return total_eager(s, o, out, far, near_images);
+  } catch (...) {  // a host-side check of the call (argument / validation error): propagate
+    abandon();
     throw;
   }
   defer_ = false;
-  cuda_check(cudaStreamEndCapture(capture_stream_, &graph), "end capture");
+  cudaError_t err = cudaStreamEndCapture(capture_stream_, &graph);
+  if (err == cudaSuccess) err = cudaGraphInstantiate(&e.exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    count_launches(-(launch_count() - l0));
+    pending_.clear();
+    no_graph_.push_back(k);
+    return total_eager(s, o, out, far, near_images);
+  }
   e.launches = launch_count() - l0;
   count_launches(-e.launches);  // captured, not run: counted on every replay instead
   e.far_timed = far_timed_;
   e.near_timed = near_timed_;
   e.checks = std::move(pending_);
   pending_.clear();
-  cudaError_t err = cudaGraphInstantiate(&e.exec, graph, 0);
-  cudaGraphDestroy(graph);
-  cuda_check(err, "graph instantiate");
   if (graph_epoch_ != buffer_epoch()) {  // the capture itself grew a workspace: replay later
     cudaGraphExecDestroy(e.exec);
     graph_epoch_ = buffer_epoch();

@@ -260,6 +260,7 @@ class Plan {
   std::vector<std::function<void()>> pending_;  // deferred checks of the call being captured
   std::vector<GraphEntry> graphs_;
   std::vector<GraphKey> seen_;
+  std::vector<GraphKey> no_graph_;  // shapes whose capture failed: eager from then on
   unsigned long graph_epoch_ = 0;
   cudaStream_t capture_stream_ = nullptr;
   // parallel branches of a captured call: [0] validation, [1] the near tile
