@@ -55,7 +55,7 @@ std::string list(const std::vector<double>& v) {
 }  // namespace
 
 // --cache-check: the drop-in API's per-periodizer plan cache (api.cu PlanCache, 8 entries)
-// under eviction. 12 distinct periodizers (3 cells x 4 eps) are applied round-robin three
+// under eviction. 12 distinct periodizers (3 cell heights x 4 eps) are applied round-robin three
 // times to a small system; every result must equal, bitwise, the first result of the same
 // periodizer (a rebuilt plan after eviction is the same deterministic computation), and a
 // periodizer copied by value must hit the same plan. Prints one JSON line; exit 1 on mismatch.
@@ -73,10 +73,10 @@ int cache_check() {
   for (auto& q : sys.charges) q -= mean / n;
   sys.targets = sys.sources;
   std::vector<periwave::Periodizer> pzs;
-  for (double xi : {0.0, 0.2, -0.3})
+  for (double eta : {0.8, 1.0, 1.3})  // |y| <= 0.4: the points lie in all three cells
     for (double eps : {1e-6, 1e-8, 1e-10, 1e-12})
       pzs.push_back(periwave::make_periodizer(periwave::Pde::Poisson, 0.0,
-                                              periwave::make_unit_cell(1.0, xi, 0.8, periwave::Periodicity::Doubly), eps));
+                                              periwave::make_unit_cell(1.0, 0.0, eta, periwave::Periodicity::Doubly), eps));
   std::vector<std::vector<double>> first(pzs.size());
   int mismatches = 0, calls = 0;
   for (int round = 0; round < 3; ++round)
