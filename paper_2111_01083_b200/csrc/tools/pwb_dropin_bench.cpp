@@ -73,7 +73,7 @@ int cache_check() {
   for (auto& q : sys.charges) q -= mean / n;
   sys.targets = sys.sources;
   std::vector<periwave::Periodizer> pzs;
-  for (double eta : {0.8, 1.0, 1.3})  // |y| <= 0.4: the points lie in all three cells
+  for (double eta : {0.8, 0.9, 1.0})  // |y| <= 0.4: the points lie in all three cells (d >= |e2|)
     for (double eps : {1e-6, 1e-8, 1e-10, 1e-12})
       pzs.push_back(periwave::make_periodizer(periwave::Pde::Poisson, 0.0,
                                               periwave::make_unit_cell(1.0, 0.0, eta, periwave::Periodicity::Doubly), eps));
