@@ -43,6 +43,14 @@ __global__ void gather_kernel(const T* __restrict__ in, const int* __restrict__ 
   if (i < n) out[i] = in[perm[i]];
 }
 
+__global__ void gather_scale_kernel(const double2* __restrict__ in, const int* __restrict__ perm, size_t n, double sc,
+                                    double2* __restrict__ out) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 p = in[perm[i]];
+  out[i] = make_double2(p.x * sc, p.y * sc);
+}
+
 unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
 // out[perm[i] * w + k] += in[i * w + k]: sorted-order fixed-point rows back to input order
@@ -103,6 +111,12 @@ void scatter_add_rows(const unsigned long long* in, const int* perm, size_t n, i
 void gather_double2(const double2* in, const int* perm, size_t n, double2* out, cudaStream_t st) {
   if (n == 0 || in == nullptr) return;
   gather_kernel<double2><<<blocks_for(n), 256, 0, st>>>(in, perm, n, out);
+  count_launches(1);
+}
+
+void gather_scale_double2(const double2* in, const int* perm, size_t n, double sc, double2* out, cudaStream_t st) {
+  if (n == 0 || in == nullptr) return;
+  gather_scale_kernel<<<blocks_for(n), 256, 0, st>>>(in, perm, n, sc, out);
   count_launches(1);
 }
 

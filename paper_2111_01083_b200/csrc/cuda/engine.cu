@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -873,6 +874,7 @@ bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
 
 double screen_cutoff(double eps, int images, size_t ns, bool grad);
 bool near_screened(NearKind nk, const NearArgs& a);
+bool prod_form(NearKind nk, NearArgs& a, double d, size_t n);
 
 NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
                          bool identity, NearArgs& a) const {
@@ -1074,7 +1076,8 @@ int Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsi
   // same points identically, so the work items cover the same pairs); the tile runs into a
   // sorted-order scratch accumulator that is added back in input order, keeping the
   // accumulator layout (and the reduce-scatter slices) of the caller
-  if (near_screened(nk, a) && s.nt >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr) {
+  if (prod_form(nk, a, pz_.cell.d, s.nt) ||
+      (near_screened(nk, a) && s.nt >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)) {
     bin_inputs(s, a, st);
     const int* perm = a.out_row;
     a.out_row = nullptr;
@@ -1107,6 +1110,22 @@ void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, 
   cuda_check(cudaStreamSynchronize(stream_for(o)), "sync");
 }
 
+// Product form of the symmetric Laplace tile (near_sym_impl.cuh SymLaplace PROD): one image
+// row of three (singly periodic), a reduced precision tier, and a period d that is a power
+// of two, so that scaling the points by 2 / d is exact. Sets the tile's constants; the
+// caller bins (bin_inputs scales the gathered points). PWB_NO_PROD=1: off (A/B, tests).
+bool prod_form(NearKind nk, NearArgs& a, double d, size_t n) {
+  if (nk != NearKind::Laplace || !a.lowp || a.nxi != 3 || a.nrow != 1 || n < 4096) return false;
+  if (std::getenv("PWB_NO_PROD") != nullptr || std::getenv("PWB_NO_BINNING") != nullptr) return false;
+  int e = 0;
+  if (!(d > 0.0) || std::frexp(d, &e) != 0.5 || e < -400 || e > 400) return false;
+  a.prod_sc = std::ldexp(1.0, 2 - e);  // 2 / d
+  const double lnsc = static_cast<double>(2 - e) * 0.6931471805599453094;
+  a.prod_log_off = 4.0 * 0.6931471805599453094 - 6.0 * lnsc;  // ln(16 / sc^6)
+  a.prod_ln_sc2 = 2.0 * lnsc;
+  return true;
+}
+
 bool near_screened(NearKind nk, const NearArgs& a) {
   return nk == NearKind::ModHelm || nk == NearKind::ModHelmGrad || nk == NearKind::ModStokes ||
          nk == NearKind::ModStokesP || (nk == NearKind::Multipole && a.screened);
@@ -1127,7 +1146,10 @@ void Plan::bin_inputs(const DevSys& s, NearArgs& a, cudaStream_t st) {
   int* ps = bin_perm_s_.as<int>(s.ns);
   morton_order(a.src, s.ns, box, ps, ws, ws_bytes, st);
   double2* src = bin_src_.as<double2>(s.ns);
-  gather_double2(a.src, ps, s.ns, src, st);
+  if (a.prod_sc != 0.0)
+    gather_scale_double2(a.src, ps, s.ns, a.prod_sc, src, st);
+  else
+    gather_double2(a.src, ps, s.ns, src, st);
   if (a.q) {
     double* q = bin_q_.as<double>(s.ns);
     gather_double(a.q, ps, s.ns, q, st);
@@ -1150,7 +1172,10 @@ void Plan::bin_inputs(const DevSys& s, NearArgs& a, cudaStream_t st) {
     int* pt = bin_perm_t_.as<int>(s.nt);
     morton_order(a.tgt, s.nt, box, pt, ws, ws_bytes, st);
     double2* tgt = bin_tgt_.as<double2>(s.nt);
-    gather_double2(a.tgt, pt, s.nt, tgt, st);
+    if (a.prod_sc != 0.0)
+      gather_scale_double2(a.tgt, pt, s.nt, a.prod_sc, tgt, st);
+    else
+      gather_double2(a.tgt, pt, s.nt, tgt, st);
     a.tgt = tgt;
     a.out_row = pt;
   }
@@ -1176,7 +1201,10 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   record(2, branch_ ? side_[1] : st);  // on the branch the tile starts at the fork
   // screened kernels branch on beta*r per pair: bin so the branch is warp-uniform
   const bool screened = near_screened(nk, a);
-  if (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)
+  const NearArgs plain = a;  // unbinned, unscaled: the fp64 fallback of a product-form run
+  // the product-form Laplace tile needs compact tiles (and takes its points scaled)
+  const bool prod = symmetric && prod_form(nk, a, pz_.cell.d, s.nt);
+  if (prod || (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr))
     bin_inputs(s, a, branch_ ? side_[1] : st);  // the tile's stream (captured calls never bin today)
   bool done = false;
   if (symmetric) {
@@ -1188,6 +1216,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
     launch_fx_maxhi(a, maxhi, st);
     a.fx_maxhi = maxhi;
     done = launch_near_sym(nk, a, st, fx, rs_dev, rs_host, SymRange{});
+    if (prod && !done) throw_internal("product-form Laplace tile not launched");
   }
   if (!done) {
     double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
@@ -1220,7 +1249,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
     // field on the one-sided tile, which sums in fp64 like the reference
     cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset flag");
     double* ws = near_partial_.as<double>(static_cast<size_t>(kMaxSplits) * s.nt * nout);
-    launch_near(nk, a, st, ws, sms_);
+    launch_near(nk, prod ? plain : a, st, ws, sms_);
     cuda_check(cudaEventRecord(ev_[3], st), "event");
     cuda_check(cudaGetLastError(), "near launch");
     cuda_check(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");

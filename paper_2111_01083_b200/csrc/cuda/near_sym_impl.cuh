@@ -143,12 +143,34 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v, const Ne
 // values():      careful per-image semantics (slow path included, sets `flag`);
 // values_fast(): branch-free, only valid when `bad` stays 0 (FAST kernels).
 
-template <bool LOWP_, bool CLOG = false>  // CLOG: coarse table log (eps >= 1e-10, a.coarse_log)
+// PROD (one image row of three, binned points pre-scaled by a.prod_sc = 2 / d so the period
+// is 2): the three images' product in closed form. With u = dx^2, w = u + dy^2,
+//   r0^2 r-^2 r+^2 = w ((w + d^2)^2 - 4 d^2 u);
+// in the tile's units U = dX^2, W = U + dY^2, a = W / 4 + 1, P' = W (a^2 - U) = (sc^6 / 16) P:
+// 7 fp64 instructions (2 DADD, 2 DMUL, 3 DFMA) where the image loop needs 10, and the
+// constant factor is folded into the log table (a.prod_log_off). a^2 - U cancels where a
+// pair is close to a +-d image (absolute error ~3e-15 against 4 delta^2 at relative distance
+// delta), so only tile pairs whose bounding boxes keep every pair at least d / 8 from both
+// images take it (relative error <= 5e-14 in P, i.e. in the pair's log; the tier's budget
+// is 3e-13): prod_separated(). Every other tile pair runs the image loop on the same scaled
+// points -- (t - s) - shift scales exactly by a power of two, so its values and its exact
+// zeros are those of the unscaled points (apply.cpp:534).
+template <bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse table log (eps >= 1e-10, a.coarse_log)
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT,
                        CHUNK = 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
                        MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
-  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_;
+  static_assert(!PROD || LOWP_, "the product form belongs to the reduced tiers");
+  // product form of a separated tile pair (see above); dx, dy in the tile's units
+  template <class LK, class B>
+  __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const LK& K, B& bad) {
+    const double U = dx * dx;
+    const double W = fma(dy, dy, U);
+    const double aa = fma(W, 0.25, 1.0);
+    const double b = fma(aa, aa, -U);
+    V[0] = pwk::log_fast(W * b, K, bad);
+  }
   // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
   // blocks per SM fit
@@ -162,6 +184,14 @@ struct SymLaplace {
     for (int n = 0; n < NROW; ++n) {
       const double ry = row_dy<NXI, NROW>(dy, a, n);
       ry2[n] = ry * ry;
+    }
+    if constexpr (PROD) {
+      // scaled points: shifts -2, 0, 2; the product is sc^6 P = 16 P', the table expects P'
+      static_assert(!PROD || (NXI == 3 && NROW == 1), "one image row of three");
+      const double xm = dx + 2.0, xp = dx - 2.0;
+      const double P = (fma(xm, xm, ry2[0]) * 0x1p-4) * (fma(dx, dx, ry2[0]) * fma(xp, xp, ry2[0]));
+      V[0] = pwk::log_fast(P, K, bad);
+      return;
     }
     double P = 1.0;
 #pragma unroll
@@ -178,13 +208,15 @@ struct SymLaplace {
     double L = 0.0;
     for (int n = 0; n < NROW; ++n)
       for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = row_dy<NXI, NROW>(dy, a, n);
+        // PROD: scaled points, shift m d * sc = 2 (m - 1); each image's log carries ln sc^2
+        const double rx = PROD ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = PROD ? dy : row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
         }
         L += pwk::log_r2_safe(rx, ry);
+        if (PROD) L -= a.prod_ln_sc2;
       }
     V[0] = L;
   }
@@ -207,6 +239,7 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
   static constexpr bool CHEB = !GRAD;     // regime 3: per-tile-pair Chebyshev K0 (pw_math.cuh cheb_fit_k0)
+  static constexpr bool PROD = false;
   static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
@@ -315,7 +348,7 @@ struct SymStokes {
                                                                                                 : PWB_SYM_STOKES_TPT,
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
                        LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
-  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = false;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -480,6 +513,18 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
   return mask;
 }
 
+// Product-form Laplace tile (SymLaplace PROD): whether every pair between the row box and
+// the column box stays at least a quarter unit (d / 8: the period is 2 in the tile's units)
+// away from both the +2 and the -2 image, in x or in y. Boxes are (xmin, -xmax, ymin, -ymax).
+__device__ __forceinline__ bool prod_separated(const double* tb, const double* sb) {
+  const double xlo = tb[0] + sb[1], xhi = -tb[1] - sb[0];  // range of t.x - s.x
+  const double ylo = tb[2] + sb[3], yhi = -tb[3] - sb[2];
+  const double gy = ylo > 0.0 ? ylo : (yhi < 0.0 ? -yhi : 0.0);
+  const double gp = xlo > 2.0 ? xlo - 2.0 : (xhi < 2.0 ? 2.0 - xhi : 0.0);    // gap to +2
+  const double gm = xlo > -2.0 ? xlo + 2.0 : (xhi < -2.0 ? -2.0 - xhi : 0.0);  // gap to -2
+  return fmax(fmin(gp, gm), gy) >= 0.25;
+}
+
 template <class K, int NXI, int NROW, bool USK>
 __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   constexpr int TPT = K::TPT;
@@ -531,15 +576,18 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   using LKT = std::conditional_t<kTab, pwk::LogT<kRepl, kBits>, pwk::LogK<K::LOWP>>;
   LKT LK;
   if constexpr (kTab) {
-    pwk::log_tab_fill<kRepl, kBits>(s_lt, tid, kT);  // visible after the first __syncthreads of the tile loop
+    // visible after the first __syncthreads of the tile loop
+    pwk::log_tab_fill<kRepl, kBits>(s_lt, tid, kT, K::PROD ? a.prod_log_off : 0.0);
     LK = pwk::log_tab_consts<kRepl, kBits>(s_lt, lane);
   } else if constexpr (K::FAST) {
     LK = pwk::log_consts<K::LOWP>();
   }
   if constexpr (K::EXP_TAB) pwk::exp_tab_fill();  // visible after the first __syncthreads of the tile loop
   // screened kernels: bounding boxes of the row tile and of each column tile -> image mask
-  __shared__ double s_rbox[K::CULL ? kWarps : 1][4], s_cbox[K::CULL ? kWarps : 1][4];
-  if constexpr (K::CULL) {
+  constexpr bool kBoxes = K::CULL || K::PROD;  // PROD: which tile pairs may take the product form
+  static_assert(!K::PROD || kTab, "the product form's constant factor lives in the log table");
+  __shared__ double s_rbox[kBoxes ? kWarps : 1][4], s_cbox[kBoxes ? kWarps : 1][4];
+  if constexpr (kBoxes) {
     double b[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
     for (int k = 0; k < TPT; ++k)
@@ -562,7 +610,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       const double2 p = lv ? a.src[j] : make_double2(0.0, 0.0);
       s_x[i] = p.x;
       s_y[i] = p.y;
-      if (K::CULL && lv) {
+      if (kBoxes && lv) {
         cb[0] = fmin(cb[0], p.x);
         cb[1] = fmin(cb[1], -p.x);
         cb[2] = fmin(cb[2], p.y);
@@ -577,16 +625,18 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 #pragma unroll
         for (int wv = 0; wv < kWarps; ++wv) s_col[wv][c][i] = 0.0;
     }
-    if constexpr (K::CULL) warp_box_store(cb[0], cb[1], cb[2], cb[3], lane, s_cbox[warp]);
+    if constexpr (kBoxes) warp_box_store(cb[0], cb[1], cb[2], cb[3], lane, s_cbox[warp]);
     __syncthreads();
     unsigned mask = ~0u;
     double rb[4], cbx[4];
-    if (K::CULL && a.cull) {
+    if (kBoxes && (K::PROD || a.cull)) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         rb[c] = fmin(fmin(s_rbox[0][c], s_rbox[1][c]), fmin(s_rbox[2][c], s_rbox[3][c]));
         cbx[c] = fmin(fmin(s_cbox[0][c], s_cbox[1][c]), fmin(s_cbox[2][c], s_cbox[3][c]));
       }
+    }
+    if (K::CULL && a.cull) {
       mask = image_mask<NXI, NROW>(rb, cbx, a);
       if (mask == 0u) continue;  // block-uniform: no pair of this tile pair is in range
     }
@@ -710,26 +760,39 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
             keep[k][c] = racc[k][c];
         }
       std::conditional_t<kTab, unsigned, int> bad = 0;  // see pwk::log_bad
+      auto fast_loop = [&](auto prod) {
 #pragma unroll K::UNROLL
-      for (int i = 0; i < CT; ++i) {
-        const int jj = (lane + i) & (CT - 1);
-        const double sx = s_x[jj], sy = s_y[jj];
-        double w[K::NW];
+        for (int i = 0; i < CT; ++i) {
+          const int jj = (lane + i) & (CT - 1);
+          const double sx = s_x[jj], sy = s_y[jj];
+          double w[K::NW];
 #pragma unroll
-        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
-        double cacc[K::NACC];
+          for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+          double cacc[K::NACC];
 #pragma unroll
-        for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+          for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
 #pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          double V[K::NV];
-          // (t - s) - shift as upstream (apply.cpp:534)
-          K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
-          K::row(racc[k], V, w);
-          K::col(cacc, V, tw[k]);
+          for (int k = 0; k < TPT; ++k) {
+            double V[K::NV];
+            // (t - s) - shift as upstream (apply.cpp:534)
+            if constexpr (decltype(prod)::value)
+              K::values_prod(V, tx[k] - sx, ty[k] - sy, LK, bad);
+            else
+              K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
+            K::row(racc[k], V, w);
+            K::col(cacc, V, tw[k]);
+          }
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
         }
-#pragma unroll
-        for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+      };
+      if constexpr (K::PROD) {
+        if (prod_separated(rb, cbx))  // block-uniform
+          fast_loop(std::true_type{});
+        else
+          fast_loop(std::false_type{});
+      } else {
+        fast_loop(std::false_type{});
       }
       if (__syncthreads_or(pwk::log_bad(LK, bad))) {  // rare: redo this tile on the careful path
 #pragma unroll

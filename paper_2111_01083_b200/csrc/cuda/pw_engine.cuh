@@ -88,6 +88,12 @@ struct NearArgs {
   int coarse_log = 0;            // symmetric Laplace / Stokeslet tiles: 256-entry table log (eps >= 1e-10)
   double cheb_tol = 0.0;         // screened symmetric tile: per-tile-pair Chebyshev K0 fit (0: off)
   double inv_beta2 = 0.0;
+  // Product-form symmetric Laplace tile (one image row, near_sym_impl.cuh SymLaplace PROD):
+  // src / tgt hold the binned points times prod_sc = 2 / d, an exact power of two (0: off),
+  // so the period is 2 in the tile's units
+  double prod_sc = 0.0;
+  double prod_log_off = 0.0;     // ln(16 / prod_sc^6): added to the log table's entries
+  double prod_ln_sc2 = 0.0;      // ln(prod_sc^2): one image's log offset on the careful path
   // host side only: a split one-sided tile may run on its own stream (a parallel branch of a
   // captured small call, engine.cu total_eager); the partials' reduction waits for tile_done
   void* tile_stream = nullptr;
@@ -104,6 +110,8 @@ void morton_order(const double2* pts, size_t n, const BinBox& box, int* perm, vo
                   cudaStream_t st);
 void gather_double(const double* in, const int* perm, size_t n, double* out, cudaStream_t st);
 void gather_double2(const double2* in, const int* perm, size_t n, double2* out, cudaStream_t st);
+// out[i] = in[perm[i]] * sc (sc a power of two: exact)
+void gather_scale_double2(const double2* in, const int* perm, size_t n, double sc, double2* out, cudaStream_t st);
 // out[perm[i]] += in[i] row-wise (width uint64 per row): sorted fixed-point rows -> input order
 void scatter_add_rows(const unsigned long long* in, const int* perm, size_t n, int width, unsigned long long* out,
                       cudaStream_t st);
