@@ -240,6 +240,8 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
   static constexpr bool CHEB = !GRAD;     // regime 3: per-tile-pair Chebyshev K0 (pw_math.cuh cheb_fit_k0)
   static constexpr bool PROD = false;
+  template <class LK, class B>
+  __device__ __forceinline__ static void values_prod(double*, double, double, const LK&, B&) {}  // SymLaplace only
   static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
@@ -349,6 +351,8 @@ struct SymStokes {
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
                        LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = false;
+  template <class LK, class B>
+  __device__ __forceinline__ static void values_prod(double*, double, double, const LK&, B&) {}  // SymLaplace only
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
