@@ -270,8 +270,10 @@ int pwb_fast_nufft_available(void);
  * reference counterpart); 7 the near tiles' K0(x), K1(x)
  * in the full and the reduced tier (4 out, x < 64); 8 the reduced tier's table-driven
  * ln(x) (1 out); 9 K0(x), K1(x) in the symmetric screened tile's coarse tier (2 out,
- * x < 64); 10 the coarse table-driven ln(x) (1 out). Inputs per point: which 0, 6-10:
- * x (1 double); 1-4: r (2); 5: r, n (4).
+ * x < 64); 10 the coarse table-driven ln(x) (1 out); 11 the reciprocal-seeded coarse ln(x)
+ * of the product-form Laplace tile (1 out); 12 the hardware reciprocal seed of x's high
+ * word with its low 12 bits cleared (1 out). Inputs per point: which 0, 6-12: x (1 double);
+ * 1-4: r (2); 5: r, n (4).
  * Host memory. */
 int pwb_eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out);
 

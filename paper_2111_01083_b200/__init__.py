@@ -596,8 +596,8 @@ def nufft_type3(backend: NufftBackend, eps: float, x, c, s) -> np.ndarray:
 
 def eval_kernel(which: int, pde: int, beta: float, l: int, inputs: np.ndarray) -> np.ndarray:
     """Device pair math at host points (pwb_eval_kernel)."""
-    widths_in = {0: 1, 1: 2, 2: 2, 3: 2, 4: 2, 5: 4, 6: 1, 7: 1, 8: 1, 9: 1, 10: 1}
-    widths_out = {0: 1, 1: 1, 2: 4, 3: 2, 4: 2, 5: 4, 6: 6, 7: 4, 8: 1, 9: 2, 10: 1}
+    widths_in = {0: 1, 1: 2, 2: 2, 3: 2, 4: 2, 5: 4, 6: 1, 7: 1, 8: 1, 9: 1, 10: 1, 11: 1, 12: 1}
+    widths_out = {0: 1, 1: 1, 2: 4, 3: 2, 4: 2, 5: 4, 6: 6, 7: 4, 8: 1, 9: 2, 10: 1, 11: 1, 12: 1}
     a = np.ascontiguousarray(inputs, dtype=np.float64).reshape(-1)
     n = a.size // widths_in[which]
     out = np.zeros(n * widths_out[which])

@@ -732,7 +732,8 @@ int pwb_near_sym_items(const pwb_periodizer* h, size_t n, const pwb_options* o, 
   return guard([&] {
     const pwb::Opts opt = opts_from(o);
     const pwb::NearKind k = pwb::near_kind_of(h->pz, opt.with_pressure, opt.with_gradient);
-    *n_items = pwb::near_sym_item_count(k, n);
+    // the tile variant decides the work-item shape (host-only: no device needed to count)
+    *n_items = pwb::near_sym_supported(k) ? pwb::near_sym_item_count(k, n, pwb::prod_eligible(h->pz, k, n)) : 0;
     if (nout) *nout = static_cast<int>(pwb::near_outputs(k));
     return OK;
   });
@@ -819,7 +820,7 @@ int pwb_nufft_type3(int backend, double eps, size_t n, const double* x, const do
 int pwb_fast_nufft_available(void) { return 1; }
 
 int pwb_eval_kernel(int which, int pde, double beta, int l, size_t n, const double* in, double* out) {
-  if (which < 0 || which > 10) return fail_arg("unknown kernel");
+  if (which < 0 || which > 12) return fail_arg("unknown kernel");
   if (n && (!in || !out)) return fail_arg("null argument");
   return guard([&] {
     current_device(-1);

@@ -874,7 +874,7 @@ bool Plan::target_pass(const DevSys& s, const Opts& o, const double* coeff, cons
 
 double screen_cutoff(double eps, int images, size_t ns, bool grad);
 bool near_screened(NearKind nk, const NearArgs& a);
-bool prod_form(NearKind nk, NearArgs& a, double d, size_t n);
+bool prod_form(const periwave::Periodizer& pz, NearKind nk, NearArgs& a, size_t n);
 
 NearKind Plan::near_args(const DevSys& s, const Opts& o, const DevOut& out, bool single, double shx, double shy,
                          bool identity, NearArgs& a) const {
@@ -1012,7 +1012,7 @@ long Plan::sym_items(const Opts& o, size_t n) {
   NearArgs a;
   const NearKind nk = near_args(s, o, DevOut{}, false, 0, 0, false, a);
   if (!near_sym_supported(nk) || n == 0) return 0;
-  return near_sym_item_count(nk, n);
+  return near_sym_item_count(nk, n, prod_form(pz_, nk, a, n));
 }
 
 // Screened kernels (binned, masked, regime sweeps) cost very different amounts per work
@@ -1023,7 +1023,7 @@ void Plan::sym_split(const DevSys& s, const Opts& o, int world, long* bounds) {
   require(world >= 1 && world <= 64, ErrorCode::Unsupported, "world size must be in [1, 64]");
   NearArgs a;
   const NearKind nk = near_args(s, o, DevOut{}, false, 0, 0, false, a);
-  const long items = near_sym_supported(nk) ? near_sym_item_count(nk, s.nt) : 0;
+  const long items = near_sym_supported(nk) ? near_sym_item_count(nk, s.nt, prod_form(pz_, nk, a, s.nt)) : 0;
   const bool screened = near_screened(nk, a) && s.nt >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr &&
                         std::getenv("PWB_COUNT_SPLIT") == nullptr;
   if (!screened || world == 1 || items == 0) {
@@ -1076,7 +1076,7 @@ int Plan::sym_partial(const DevSys& s, const Opts& o, long begin, long end, unsi
   // same points identically, so the work items cover the same pairs); the tile runs into a
   // sorted-order scratch accumulator that is added back in input order, keeping the
   // accumulator layout (and the reduce-scatter slices) of the caller
-  if (prod_form(nk, a, pz_.cell.d, s.nt) ||
+  if (prod_form(pz_, nk, a, s.nt) ||
       (near_screened(nk, a) && s.nt >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr)) {
     bin_inputs(s, a, st);
     const int* perm = a.out_row;
@@ -1111,14 +1111,22 @@ void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, 
 }
 
 // Product form of the symmetric Laplace tile (near_sym_impl.cuh SymLaplace PROD): one image
-// row of three (singly periodic), a reduced precision tier, and a period d that is a power
-// of two, so that scaling the points by 2 / d is exact. Sets the tile's constants; the
-// caller bins (bin_inputs scales the gathered points). PWB_NO_PROD=1: off (A/B, tests).
-bool prod_form(NearKind nk, NearArgs& a, double d, size_t n) {
-  if (nk != NearKind::Laplace || !a.lowp || a.nxi != 3 || a.nrow != 1 || n < 4096) return false;
+// row of three (singly periodic), a reduced precision tier (eps >= 1e-11), and a period d
+// that is a power of two, so that scaling the points by 2 / d is exact. Host-only (the
+// work-item count of pwb_near_sym_items needs no device). PWB_NO_PROD=1: off (A/B, tests).
+bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
+  if (nk != NearKind::Laplace || pz.cell.periodicity != periwave::Periodicity::Singly || n < 4096) return false;
+  if (!(pz.eps >= 1e-11) || std::getenv("PWB_FULL_PRECISION") != nullptr) return false;
   if (std::getenv("PWB_NO_PROD") != nullptr || std::getenv("PWB_NO_BINNING") != nullptr) return false;
   int e = 0;
-  if (!(d > 0.0) || std::frexp(d, &e) != 0.5 || e < -400 || e > 400) return false;
+  const double d = pz.cell.d;
+  return d > 0.0 && std::frexp(d, &e) == 0.5 && e >= -400 && e <= 400;
+}
+// Sets the tile's constants when eligible; the caller bins (bin_inputs scales the gathered points).
+bool prod_form(const periwave::Periodizer& pz, NearKind nk, NearArgs& a, size_t n) {
+  if (!prod_eligible(pz, nk, n) || !a.lowp || a.nxi != 3 || a.nrow != 1) return false;
+  int e = 0;
+  std::frexp(pz.cell.d, &e);
   a.prod_sc = std::ldexp(1.0, 2 - e);  // 2 / d
   const double lnsc = static_cast<double>(2 - e) * 0.6931471805599453094;
   a.prod_log_off = 4.0 * 0.6931471805599453094 - 6.0 * lnsc;  // ln(16 / sc^6)
@@ -1203,7 +1211,7 @@ void Plan::near(const DevSys& s, const Opts& o, const DevOut& out, bool single, 
   const bool screened = near_screened(nk, a);
   const NearArgs plain = a;  // unbinned, unscaled: the fp64 fallback of a product-form run
   // the product-form Laplace tile needs compact tiles (and takes its points scaled)
-  const bool prod = symmetric && prod_form(nk, a, pz_.cell.d, s.nt);
+  const bool prod = symmetric && prod_form(pz_, nk, a, s.nt);
   if (prod || (!single && screened && s.nt >= 4096 && s.ns >= 4096 && std::getenv("PWB_NO_BINNING") == nullptr))
     bin_inputs(s, a, branch_ ? side_[1] : st);  // the tile's stream (captured calls never bin today)
   bool done = false;

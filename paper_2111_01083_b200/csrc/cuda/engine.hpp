@@ -100,6 +100,8 @@ enum class Kind { Scalar, Velocity, Multipole };
 Kind kind_of(const periwave::Periodizer& pz);
 // which near-field tile the periodizer and options select (host only)
 NearKind near_kind_of(const periwave::Periodizer& pz, bool with_pressure, bool with_gradient);
+// whether the symmetric near field of n points takes the product-form Laplace tile (host-only)
+bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n);
 
 // One family of plane-wave parts that share a weight set and output shape.
 struct Family {

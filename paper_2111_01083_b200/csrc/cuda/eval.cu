@@ -155,6 +155,14 @@ __global__ void eval_kernel(int which, int pde, double beta, int l, size_t n, co
       out[i] = pwk::log_tab<1>(in[i], pwk::log_tab_consts<1, 8>(pwk::pw_log_tab_dev_ptr<8>(), 0), bad);
       break;
     }
+    case 11: {  // the reciprocal-seeded table log (pw_math.cuh log_seed), entries computed in place
+      unsigned bad = 0;
+      out[i] = pwk::log_seed<0, 8>(in[i], pwk::log_seed_consts<1, 8>(nullptr, 0), bad);
+      break;
+    }
+    case 12:  // the hardware reciprocal seed of the operand's high word with the low 12 bits cleared
+      out[i] = pwk::rcp_seed(static_cast<unsigned>(pwk::hi_of(in[i])) & 0xfffff000u);
+      break;
     default:
       out[i] = nan("");
   }
@@ -212,7 +220,7 @@ double fp64_peak_probe() {
 
 int eval_in_width(int which) { return (which == 0 || which >= 6) ? 1 : which == 5 ? 4 : 2; }
 int eval_out_width(int which) {
-  return (which <= 1 || which == 8 || which == 10) ? 1 : (which == 3 || which == 4 || which == 9) ? 2
+  return (which <= 1 || which == 8 || which == 10 || which == 11 || which == 12) ? 1 : (which == 3 || which == 4 || which == 9) ? 2
                                                       : which == 6                              ? 6
                                                                                                 : 4;
 }

@@ -92,7 +92,7 @@ size_t near_sym_tiles(size_t n) { return (n + 127) / 128; }
 namespace {
 template <class K>
 long item_count(size_t n) {
-  const size_t tile = static_cast<size_t>(sym::kT) * K::TPT, ct = static_cast<size_t>(sym::kT) * K::CPT;
+  const size_t tile = static_cast<size_t>(K::THREADS) * K::TPT, ct = static_cast<size_t>(sym::kColUnit) * K::CPT;
   const long nb = static_cast<long>((n + tile - 1) / tile), ncb = static_cast<long>((n + ct - 1) / ct);
   const long r = static_cast<long>(tile / ct);
   long items = 0;
@@ -200,7 +200,7 @@ void near_sym_shape(NearKind kind, int* tile, int* chunk) {
   auto set = [&](auto k) {
     using K = decltype(k);
     static_assert(K::CPT == K::TPT || !K::CULL, "the cost split assumes square tiles");
-    *tile = sym::kT * K::TPT;
+    *tile = K::THREADS * K::TPT;
     *chunk = K::CHUNK;
   };
   switch (kind) {
@@ -258,9 +258,10 @@ void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_ho
   cuda_check(cudaStreamSynchronize(st), "split sync");
 }
 
-long near_sym_item_count(NearKind kind, size_t n) {
+long near_sym_item_count(NearKind kind, size_t n, bool prod) {
   switch (kind) {
-    case NearKind::Laplace: return item_count<sym::SymLaplace<false>>(n);
+    case NearKind::Laplace:  // the product-form tile has its own row tile (near_sym_impl.cuh)
+      return prod ? item_count<sym::SymLaplace<true, true, true>>(n) : item_count<sym::SymLaplace<false>>(n);
     case NearKind::ModHelm: return item_count<sym::SymModHelm<false, false>>(n);
     case NearKind::ModHelmGrad: return item_count<sym::SymModHelm<true, false>>(n);
     case NearKind::Stokes: return item_count<sym::SymStokes<false, false>>(n);

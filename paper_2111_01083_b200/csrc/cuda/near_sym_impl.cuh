@@ -101,10 +101,20 @@ namespace sym {
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 8  // 8 x 4 warps/SM at 64 registers (the cold careful path spills 32 B): c4 near 637.3 / 639.1 -> 632.9 / 632.7 ms vs 7 (r2i, r2j); 7 beat 6 (667 -> 653)
 #endif
-constexpr int kT = 128;  // threads per block
+#ifndef PWB_SYM_PROD_THREADS
+#define PWB_SYM_PROD_THREADS 128  // threads per block of the product-form Laplace tile (A/B r2w: 256 with one 8-replica table per 8 warps 608 ms vs 572)
+#endif
+#ifndef PWB_SYM_PROD_REPL
+#define PWB_SYM_PROD_REPL 4  // its log-table replicas (as PWB_SYM_CLOG_REPL)
+#endif
+#ifndef PWB_SYM_PROD_SEED
+#define PWB_SYM_PROD_SEED 0  // 1: reciprocal-seeded 8-byte table (pw_math.cuh log_seed): half the table bytes, +2.8 instructions per pair; A/B r2w 599 ms vs 572 (the tile is issue-bound, not shared-memory-bound)
+#endif
+// Threads per block: K::THREADS (128 unless a functor says otherwise); a row tile is
+// K::THREADS * K::TPT points, a column tile kColUnit * K::CPT points.
+constexpr int kColUnit = 128;
 constexpr int kSymMhUnrollM = PWB_SYM_MH_UNROLL_M;
 constexpr int kSymMhSrcUnroll = PWB_SYM_MH_SRC_UNROLL;
-constexpr int kWarps = kT / 32;
 
 // ---------------------------------------------------------------- fixed point
 // v = a 2^22 + b 2^-20 + c 2^-62; limbs truncate toward zero so each carries the
@@ -159,8 +169,14 @@ template <bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse ta
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT,
                        CHUNK = 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
-                       MINB = PWB_SYM_LAPLACE_MINB, UNROLL = PWB_SYM_LAPLACE_UNROLL;
+                       MINB = PROD_ ? PWB_SYM_LAPLACE_MINB * 128 / PWB_SYM_PROD_THREADS : PWB_SYM_LAPLACE_MINB,
+                       UNROLL = PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_;
+  // PROD: 256 threads share one conflict-free 8-replica table (32 KB at 256 entries): the
+  // tile is bound by shared-memory wavefronts next to the fp64 pipe (ncu r2s: 86 % / 68 %),
+  // and the 4-replica table's bank conflicts cost 2.4 of its 9.2 wavefronts per warp and pair
+  static constexpr int THREADS = PROD_ ? PWB_SYM_PROD_THREADS : 128;
+  static constexpr bool LOG_SEED = PROD_ && PWB_SYM_PROD_SEED;  // table type: pwk::LogR instead of pwk::LogT
   static_assert(!PROD || LOWP_, "the product form belongs to the reduced tiers");
   // product form of a separated tile pair (see above); dx, dy in the tile's units
   template <class LK, class B>
@@ -174,7 +190,8 @@ struct SymLaplace {
   // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
   // blocks per SM fit
-  static constexpr int CPT = PWB_SYM_LAPLACE_CPT, LOG_REPL = CLOG ? PWB_SYM_CLOG_REPL : PWB_SYM_LAPLACE_REPL,
+  static constexpr int CPT = PWB_SYM_LAPLACE_CPT,
+                       LOG_REPL = PROD_ ? PWB_SYM_PROD_REPL : (CLOG ? PWB_SYM_CLOG_REPL : PWB_SYM_LAPLACE_REPL),
                        LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;  // 256 x 4 x 16 B = 16 KB
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -239,7 +256,8 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool EXP_TAB = LOWP_;  // k01_tile<true, .> reads the shared exp table
   static constexpr bool CULL = true;      // per-tile image mask from bounding boxes (see near_sym_body)
   static constexpr bool CHEB = !GRAD;     // regime 3: per-tile-pair Chebyshev K0 (pw_math.cuh cheb_fit_k0)
-  static constexpr bool PROD = false;
+  static constexpr bool PROD = false, LOG_SEED = false;
+  static constexpr int THREADS = 128;
   template <class LK, class B>
   __device__ __forceinline__ static void values_prod(double*, double, double, const LK&, B&) {}  // SymLaplace only
   static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
@@ -350,7 +368,8 @@ struct SymStokes {
                                                                                                 : PWB_SYM_STOKES_TPT,
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
                        LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
-  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = false;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = false, LOG_SEED = false;
+  static constexpr int THREADS = 128;
   template <class LK, class B>
   __device__ __forceinline__ static void values_prod(double*, double, double, const LK&, B&) {}  // SymLaplace only
   template <int NXI, int NROW, bool USK, class LK, class B>
@@ -532,8 +551,9 @@ __device__ __forceinline__ bool prod_separated(const double* tb, const double* s
 template <class K, int NXI, int NROW, bool USK>
 __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   constexpr int TPT = K::TPT;
-  constexpr int TILE = kT * TPT;      // row tile: the block's targets
-  constexpr int CT = kT * K::CPT;     // column tile: the sources staged per step
+  constexpr int kT = K::THREADS, kWarps = kT / 32;
+  constexpr int TILE = kT * TPT;          // row tile: the block's targets
+  constexpr int CT = kColUnit * K::CPT;   // column tile: the sources staged per step
   constexpr int R = TILE / CT;        // column tiles per row tile
   static_assert(TILE % CT == 0 && (CT & (CT - 1)) == 0, "column tile must divide the row tile");
   const NearArgs& a = S.a;
@@ -574,12 +594,19 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
   // log constants in registers; the reduced tier's log table in shared memory
   constexpr size_t kTileSmem = sizeof(double) * (static_cast<size_t>(CT) * (2 + K::NW) + kWarps * K::NACC * CT);
   constexpr int kRepl = K::LOG_REPL, kBits = K::LOG_BITS;
-  constexpr size_t kTabSmem = sizeof(double2) * (size_t{1} << pwk::tab_bits(kBits)) * kRepl;
+  constexpr size_t kTabEntry = K::LOG_SEED ? sizeof(double) : sizeof(double2);
+  constexpr size_t kTabSmem = kTabEntry * (size_t{1} << pwk::tab_bits(kBits)) * kRepl;
   constexpr bool kTab = K::FAST && K::LOWP && PWB_SYM_LOG_TABLE && kTileSmem + kTabSmem <= 48 * 1024;
-  __shared__ double2 s_lt[kTab ? (1 << pwk::tab_bits(kBits)) * kRepl : 1];
-  using LKT = std::conditional_t<kTab, pwk::LogT<kRepl, kBits>, pwk::LogK<K::LOWP>>;
+  __shared__ double2 s_lt[kTab ? kTabSmem / sizeof(double2) : 1];
+  using LKT = std::conditional_t<kTab,
+                                 std::conditional_t<K::LOG_SEED, pwk::LogR<kRepl, kBits>, pwk::LogT<kRepl, kBits>>,
+                                 pwk::LogK<K::LOWP>>;
   LKT LK;
-  if constexpr (kTab) {
+  if constexpr (kTab && K::LOG_SEED) {
+    // visible after the first __syncthreads of the tile loop
+    pwk::log_seed_fill<kRepl, kBits>(reinterpret_cast<double*>(s_lt), tid, kT, K::PROD ? a.prod_log_off : 0.0);
+    LK = pwk::log_seed_consts<kRepl, kBits>(reinterpret_cast<const double*>(s_lt), lane);
+  } else if constexpr (kTab) {
     // visible after the first __syncthreads of the tile loop
     pwk::log_tab_fill<kRepl, kBits>(s_lt, tid, kT, K::PROD ? a.prod_log_off : 0.0);
     LK = pwk::log_tab_consts<kRepl, kBits>(s_lt, lane);
@@ -636,8 +663,18 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     if (kBoxes && (K::PROD || a.cull)) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        rb[c] = fmin(fmin(s_rbox[0][c], s_rbox[1][c]), fmin(s_rbox[2][c], s_rbox[3][c]));
-        cbx[c] = fmin(fmin(s_cbox[0][c], s_cbox[1][c]), fmin(s_cbox[2][c], s_cbox[3][c]));
+        if constexpr (kWarps == 4) {
+          rb[c] = fmin(fmin(s_rbox[0][c], s_rbox[1][c]), fmin(s_rbox[2][c], s_rbox[3][c]));
+          cbx[c] = fmin(fmin(s_cbox[0][c], s_cbox[1][c]), fmin(s_cbox[2][c], s_cbox[3][c]));
+        } else {
+          rb[c] = s_rbox[0][c];
+          cbx[c] = s_cbox[0][c];
+#pragma unroll
+          for (int wv = 1; wv < kWarps; ++wv) {
+            rb[c] = fmin(rb[c], s_rbox[wv][c]);
+            cbx[c] = fmin(cbx[c], s_cbox[wv][c]);
+          }
+        }
       }
     }
     if (K::CULL && a.cull) {
@@ -870,20 +907,20 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
 // image blocks hold more live shifts and get at most 4 -- 80 or 96 regs spill there).
 // MINB == 0 keeps ptxas's own allocation (the wider functors).
 template <class K, int NXI, int NROW, bool USK>
-__global__ void __launch_bounds__(kT, NROW == 1 ? K::MINB : (K::MINB < 4 ? K::MINB : 4))
+__global__ void __launch_bounds__(K::THREADS, NROW == 1 ? K::MINB : (K::MINB < 4 ? K::MINB : 4))
     near_sym_kernel_capped(const __grid_constant__ SymArgs S) {
   near_sym_body<K, NXI, NROW, USK>(S);
 }
 
 template <class K, int NXI, int NROW, bool USK>
-__global__ void __launch_bounds__(kT) near_sym_kernel(const __grid_constant__ SymArgs S) {
+__global__ void __launch_bounds__(K::THREADS) near_sym_kernel(const __grid_constant__ SymArgs S) {
   near_sym_body<K, NXI, NROW, USK>(S);
 }
 
 template <class K, int NXI, int NROW, bool USK = false>
 void launch_sym_shape(const NearArgs& a, cudaStream_t st, unsigned long long* fx, long long* row_start_dev,
                       long long* row_start_host, const SymRange& range) {
-  constexpr int TILE = kT * K::TPT, CT = kT * K::CPT, R = TILE / CT;
+  constexpr int kT = K::THREADS, TILE = kT * K::TPT, CT = kColUnit * K::CPT, R = TILE / CT;
   const int chunk = K::CHUNK;
   const int nb = static_cast<int>((a.nt + TILE - 1) / TILE);
   const int ncb = static_cast<int>((a.nt + CT - 1) / CT);

@@ -143,7 +143,8 @@ void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int 
                       const int* out_row, const unsigned* maxhi_dev, size_t n_src, int k_host, const int* flag,
                       cudaStream_t st);
 // host-only: number of work items of the symmetric decomposition (0 if none)
-long near_sym_item_count(NearKind kind, size_t n);
+// (prod: the product-form Laplace tile, NearArgs::prod_sc != 0)
+long near_sym_item_count(NearKind kind, size_t n, bool prod = false);
 // Tile size (points) and column tiles per work item of the symmetric tile of `kind`.
 void near_sym_shape(NearKind kind, int* tile, int* chunk);
 // Cost-balanced item boundaries (world + 1 longs, host) for the screened symmetric tiles:

@@ -562,6 +562,43 @@ def test_hot_tile_coarse_table_log(pw, gpu):
     assert np.all(err <= 1e-12 + 4e-16 * np.abs(want)), err.max()
 
 
+def test_hot_tile_rcp_seed(pw, gpu):
+    """The reciprocal-seeded table log (pw_math.cuh log_seed) relies on MUFU.RCP64H being a
+    pure function of the operand's high word whose mantissa does not depend on the exponent:
+    seed(2^E c) == 2^-E seed(c) bit for bit, for every table centre c = 1 + i / 256 and a
+    range of exponents; and on the seed being within 2^-20 of 1 / c."""
+    c = 1.0 + np.arange(256) / 256.0
+    base = pw.eval_kernel(12, 0, 0.0, 0, np.ascontiguousarray(c))
+    assert np.all(np.abs(base * c - 1.0) <= 2.0 ** -20)
+    lo = base.view(np.uint64) & np.uint64(0xFFFFFFFF)
+    assert np.all(lo == 0)  # only the high word is written
+    for e in (-900, -300, -40, -7, -1, 1, 5, 60, 700):
+        got = pw.eval_kernel(12, 0, 0.0, 0, np.ascontiguousarray(np.ldexp(c, e)))
+        assert np.array_equal(np.ldexp(got, e), base), e
+    # the low 12 bits of the high word (and the low word) are ignored by the masked seed
+    x = np.nextafter(c + 1.0 / 256.0, 0.0)
+    assert np.array_equal(pw.eval_kernel(12, 0, 0.0, 0, np.ascontiguousarray(x)), base)
+
+
+def test_hot_tile_seeded_table_log(pw, gpu):
+    """The reciprocal-seeded coarse log of the product-form Laplace tile (256 centres,
+    degree-2 F, |f| <= 2^-9 + 2^-20): within 1e-12 absolute for |ln x| <= 1, against mpmath;
+    entries computed in place by the same device functions that fill the tile's table."""
+    import mpmath as mp
+
+    rng = np.random.default_rng(14)
+    edges = np.array([1.0 + (i + 0.5) / 256.0 for i in range(256)])  # rounding boundaries
+    x = np.concatenate([rng.uniform(0.5, 2.0, 4000), np.exp(rng.uniform(-45, 5, 4000)),
+                        np.exp(rng.uniform(-700, 700, 2000)),
+                        edges * 2.0 ** rng.integers(-30, 4, 256), np.nextafter(edges, 0.0), np.nextafter(edges, 4.0),
+                        np.nextafter(np.array([2.0, 1.0, 4.0, 0.5]), 0.0), np.array([1.0, 2.0, 0.5])])
+    out = pw.eval_kernel(11, 0, 0.0, 0, np.ascontiguousarray(x))
+    mp.mp.dps = 30
+    want = np.array([float(mp.log(mp.mpf(float(v)))) for v in x])
+    err = np.abs(out - want)
+    assert np.all(err <= 1e-12 + 4e-16 * np.abs(want)), err.max()
+
+
 def test_hot_tile_bessel_coarse_tier(pw, gpu, ref):
     """The symmetric screened tile's coarse tier (eps >= 1e-9, c5): 9 + 8 term asymptotic
     polynomials and a degree-3 e^r, <= ~1e-11 relative to the reference's Bessel functions."""
