@@ -101,14 +101,33 @@ namespace sym {
 #ifndef PWB_SYM_LAPLACE_MINB
 #define PWB_SYM_LAPLACE_MINB 8  // 8 x 4 warps/SM at 64 registers (the cold careful path spills 32 B): c4 near 637.3 / 639.1 -> 632.9 / 632.7 ms vs 7 (r2i, r2j); 7 beat 6 (667 -> 653)
 #endif
+// Shape of the product-form Laplace tile (SymLaplace PROD). Fewer, fatter threads than the
+// image-loop tile: with 14.25 fp64 per pair the per-source work (three LDS, the column
+// partial's read-modify-write, index arithmetic) and the dependent chains weigh more, and 8
+// targets per thread at 4 blocks/SM (128 registers) beat 4 targets at 8 blocks (A/B r3c/r3d,
+// c4 near: TPT 4 / 8 blocks / unroll 4: 571 ms; TPT 6 / 5 blocks / unroll 2: 552;
+// TPT 8 / 4 blocks: unroll 1 549, unroll 2 542, unroll 4 560; + 256-point column tiles 539;
+// TPT 10 / 3 blocks 547; TPT 12 / 3 blocks 552; TPT 16 / 2 blocks 576).
+#ifndef PWB_SYM_PROD_TPT
+#define PWB_SYM_PROD_TPT 8
+#endif
+#ifndef PWB_SYM_PROD_CPT
+#define PWB_SYM_PROD_CPT 2  // column tile 256 points
+#endif
+#ifndef PWB_SYM_PROD_MINB
+#define PWB_SYM_PROD_MINB 4
+#endif
+#ifndef PWB_SYM_PROD_UNROLL
+#define PWB_SYM_PROD_UNROLL 2
+#endif
 #ifndef PWB_SYM_PROD_THREADS
-#define PWB_SYM_PROD_THREADS 128  // threads per block of the product-form Laplace tile (A/B r2w: 256 with one 8-replica table per 8 warps 608 ms vs 572)
+#define PWB_SYM_PROD_THREADS 128  // threads per block (A/B r2w: 256 with one 8-replica table per 8 warps 608 ms vs 572)
 #endif
 #ifndef PWB_SYM_PROD_REPL
-#define PWB_SYM_PROD_REPL 4  // its log-table replicas (as PWB_SYM_CLOG_REPL)
+#define PWB_SYM_PROD_REPL 8  // log-table replicas: 8 = conflict-free LDS.128 (32 KB at 256 entries, fits 4 blocks/SM; 4: 545 vs 542 ms)
 #endif
 #ifndef PWB_SYM_PROD_SEED
-#define PWB_SYM_PROD_SEED 0  // 1: reciprocal-seeded 8-byte table (pw_math.cuh log_seed): half the table bytes, +2.8 instructions per pair; A/B r2w 599 ms vs 572 (the tile is issue-bound, not shared-memory-bound)
+#define PWB_SYM_PROD_SEED 0  // 1: reciprocal-seeded 8-byte table (pw_math.cuh log_seed): half the table bytes, +2.8 instructions per pair; A/B r2w 599 ms vs 572
 #endif
 // Threads per block: K::THREADS (128 unless a functor says otherwise); a row tile is
 // K::THREADS * K::TPT points, a column tile kColUnit * K::CPT points.
@@ -162,15 +181,16 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v, const Ne
 // pair is close to a +-d image (absolute error ~3e-15 against 4 delta^2 at relative distance
 // delta), so only tile pairs whose bounding boxes keep every pair at least d / 8 from both
 // images take it (relative error <= 5e-14 in P, i.e. in the pair's log; the tier's budget
-// is 3e-13): prod_separated(). Every other tile pair runs the image loop on the same scaled
+// is 3e-13): prod_mode(). Every other tile pair runs the image loop on the same scaled
 // points -- (t - s) - shift scales exactly by a power of two, so its values and its exact
 // zeros are those of the unscaled points (apply.cpp:534).
 template <bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse table log (eps >= 1e-10, a.coarse_log)
 struct SymLaplace {
-  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PWB_SYM_LAPLACE_TPT,
-                       CHUNK = 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
-                       MINB = PROD_ ? PWB_SYM_LAPLACE_MINB * 128 / PWB_SYM_PROD_THREADS : PWB_SYM_LAPLACE_MINB,
-                       UNROLL = PWB_SYM_LAPLACE_UNROLL;
+  static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PROD_ ? PWB_SYM_PROD_TPT : PWB_SYM_LAPLACE_TPT,
+                       CPT = PROD_ ? PWB_SYM_PROD_CPT : PWB_SYM_LAPLACE_CPT,
+                       CHUNK = PROD_ ? 32 / PWB_SYM_PROD_CPT : 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
+                       MINB = PROD_ ? PWB_SYM_PROD_MINB : PWB_SYM_LAPLACE_MINB,
+                       UNROLL = PROD_ ? PWB_SYM_PROD_UNROLL : PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_;
   // PROD: 256 threads share one conflict-free 8-replica table (32 KB at 256 entries): the
   // tile is bound by shared-memory wavefronts next to the fp64 pipe (ncu r2s: 86 % / 68 %),
@@ -190,8 +210,7 @@ struct SymLaplace {
   // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
   // blocks per SM fit
-  static constexpr int CPT = PWB_SYM_LAPLACE_CPT,
-                       LOG_REPL = PROD_ ? PWB_SYM_PROD_REPL : (CLOG ? PWB_SYM_CLOG_REPL : PWB_SYM_LAPLACE_REPL),
+  static constexpr int LOG_REPL = PROD_ ? PWB_SYM_PROD_REPL : (CLOG ? PWB_SYM_CLOG_REPL : PWB_SYM_LAPLACE_REPL),
                        LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;  // 256 x 4 x 16 B = 16 KB
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
@@ -536,16 +555,23 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
   return mask;
 }
 
-// Product-form Laplace tile (SymLaplace PROD): whether every pair between the row box and
-// the column box stays at least a quarter unit (d / 8: the period is 2 in the tile's units)
-// away from both the +2 and the -2 image, in x or in y. Boxes are (xmin, -xmax, ymin, -ymax).
-__device__ __forceinline__ bool prod_separated(const double* tb, const double* sb) {
+// Product-form Laplace tile (SymLaplace PROD), per tile pair from the row box and the column
+// box (xmin, -xmax, ymin, -ymax; the period is 2 in the tile's units):
+//   0  some pair may come within a quarter unit (d / 8) of the +2 or the -2 image in both x
+//      and y: the image loop;
+//   1  every pair stays clear of both images: the product form;
+//   2  and the boxes themselves are apart (by more than 2^-100), so no pair coincides and
+//      every product is a normal number: the product form without the exponent check and
+//      without the saved row sums of the careful redo (9 registers the loop can use).
+__device__ __forceinline__ int prod_mode(const double* tb, const double* sb) {
   const double xlo = tb[0] + sb[1], xhi = -tb[1] - sb[0];  // range of t.x - s.x
   const double ylo = tb[2] + sb[3], yhi = -tb[3] - sb[2];
   const double gy = ylo > 0.0 ? ylo : (yhi < 0.0 ? -yhi : 0.0);
+  const double gx = xlo > 0.0 ? xlo : (xhi < 0.0 ? -xhi : 0.0);
   const double gp = xlo > 2.0 ? xlo - 2.0 : (xhi < 2.0 ? 2.0 - xhi : 0.0);    // gap to +2
   const double gm = xlo > -2.0 ? xlo + 2.0 : (xhi < -2.0 ? -2.0 - xhi : 0.0);  // gap to -2
-  return fmax(fmin(gp, gm), gy) >= 0.25;
+  if (!(fmax(fmin(gp, gm), gy) >= 0.25)) return 0;
+  return fmax(gx, gy) > 0x1p-100 ? 2 : 1;
 }
 
 template <class K, int NXI, int NROW, bool USK>
@@ -787,7 +813,47 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       }
       careful = false;
     }
-    if (K::FAST) {
+    // the branch-free sweep of the staged column tile: prod selects the product form of the
+    // pair values, `bad` collects the exponent check (a local nobody reads drops it)
+    auto fast_loop = [&](auto prod, auto& bad) {
+#pragma unroll K::UNROLL
+      for (int i = 0; i < CT; ++i) {
+        const int jj = (lane + i) & (CT - 1);
+        const double sx = s_x[jj], sy = s_y[jj];
+        double w[K::NW];
+#pragma unroll
+        for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
+        double cacc[K::NACC];
+#pragma unroll
+        for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          double V[K::NV];
+          // (t - s) - shift as upstream (apply.cpp:534)
+          if constexpr (decltype(prod)::value)
+            K::values_prod(V, tx[k] - sx, ty[k] - sy, LK, bad);
+          else
+            K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
+          K::row(racc[k], V, w);
+          K::col(cacc, V, tw[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
+      }
+    };
+    using BadT = std::conditional_t<kTab, unsigned, int>;  // see pwk::log_bad
+    int pmode = 0;
+    if constexpr (K::PROD) {
+      pmode = prod_mode(rb, cbx);  // block-uniform
+      // dead rows / columns sit at the origin with weight 0: their products may vanish, so a
+      // ragged tile pair keeps the check
+      if (pmode == 2 && (static_cast<size_t>(I + 1) * TILE > n || jbase + CT > n)) pmode = 1;
+      if (pmode == 2) {
+        BadT unchecked = 0;
+        fast_loop(std::true_type{}, unchecked);
+      }
+    }
+    if (K::FAST && pmode != 2) {
       // the row sums before this tile, for the careful redo: in shared memory (each thread
       // its own column, no sync needed) when PWB_SYM_KEEP_SMEM, else in registers
       double keep[PWB_SYM_KEEP_SMEM ? 1 : TPT][K::NACC];
@@ -800,41 +866,11 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
           else
             keep[k][c] = racc[k][c];
         }
-      std::conditional_t<kTab, unsigned, int> bad = 0;  // see pwk::log_bad
-      auto fast_loop = [&](auto prod) {
-#pragma unroll K::UNROLL
-        for (int i = 0; i < CT; ++i) {
-          const int jj = (lane + i) & (CT - 1);
-          const double sx = s_x[jj], sy = s_y[jj];
-          double w[K::NW];
-#pragma unroll
-          for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][jj];
-          double cacc[K::NACC];
-#pragma unroll
-          for (int c = 0; c < K::NACC; ++c) cacc[c] = 0.0;
-#pragma unroll
-          for (int k = 0; k < TPT; ++k) {
-            double V[K::NV];
-            // (t - s) - shift as upstream (apply.cpp:534)
-            if constexpr (decltype(prod)::value)
-              K::values_prod(V, tx[k] - sx, ty[k] - sy, LK, bad);
-            else
-              K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
-            K::row(racc[k], V, w);
-            K::col(cacc, V, tw[k]);
-          }
-#pragma unroll
-          for (int c = 0; c < K::NACC; ++c) s_col[warp][c][jj] += cacc[c];
-        }
-      };
-      if constexpr (K::PROD) {
-        if (prod_separated(rb, cbx))  // block-uniform
-          fast_loop(std::true_type{});
-        else
-          fast_loop(std::false_type{});
-      } else {
-        fast_loop(std::false_type{});
-      }
+      BadT bad = 0;
+      if (K::PROD && pmode == 1)
+        fast_loop(std::true_type{}, bad);
+      else
+        fast_loop(std::false_type{}, bad);
       if (__syncthreads_or(pwk::log_bad(LK, bad))) {  // rare: redo this tile on the careful path
 #pragma unroll
         for (int k = 0; k < TPT; ++k)

@@ -224,15 +224,25 @@ def test_partitions_cover_everything():
 def test_item_counts_match_the_device_decomposition(pw):
     cell = pw.make_unit_cell(1.0, 0.0, 1.0, pw.Periodicity.Singly)
     pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-10)
-    for n, want in ((1, 1), (512, 1), (513, 2), (1000000, None)):
+    for n, want in ((1, 1), (512, 1), (513, 2), (4095, None), (4096, None), (1000000, None)):
         items, nout = pw.near_sym_items(pz, n)
-        # Laplace: 512-point row tiles (4 targets x 128 threads), 128-point column tiles,
-        # 32 column tiles (4096 sources) per item; row tile I starts at column tile 4 I
-        nb, ncb = (n + 511) // 512, (n + 127) // 128
-        assert items == sum((ncb - 4 * i + 31) // 32 for i in range(nb))
+        if n < 4096:
+            # Laplace image-loop tile: 512-point row tiles (4 targets x 128 threads), 128-point
+            # column tiles, 32 column tiles (4096 sources) per item; row tile I starts at column tile 4 I
+            nb, ncb, r, chunk = (n + 511) // 512, (n + 127) // 128, 4, 32
+        else:
+            # product-form tile (singly periodic, d a power of two, binned from 4096 points):
+            # 1024-point row tiles (8 targets x 128 threads), 256-point column tiles, 16 per item
+            nb, ncb, r, chunk = (n + 1023) // 1024, (n + 255) // 256, 4, 16
+        assert items == sum((ncb - r * i + chunk - 1) // chunk for i in range(nb))
         assert nout == 1
         if want is not None:
             assert items == want
+    # a period that is not a power of two keeps the image-loop tile's decomposition
+    pz15 = pw.make_periodizer(pw.Pde.Poisson, 0.0, pw.make_unit_cell(1.5, 0.0, 1.0, pw.Periodicity.Singly), 1e-10)
+    n = 1000000
+    nb, ncb = (n + 511) // 512, (n + 127) // 128
+    assert pw.near_sym_items(pz15, n)[0] == sum((ncb - 4 * i + 31) // 32 for i in range(nb))
     st = pw.make_periodizer(pw.Pde.Stokes, 0.0, pw.make_unit_cell(1.0, 0.0, 1.0), 1e-8)
     assert pw.near_sym_items(st, 300, pw.ApplyOptions(with_pressure=True))[1] == 3
 
