@@ -1110,27 +1110,38 @@ void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, 
   cuda_check(cudaStreamSynchronize(stream_for(o)), "sync");
 }
 
-// Product form of the symmetric Laplace tile (near_sym_impl.cuh SymLaplace PROD): one image
-// row of three (singly periodic), a reduced precision tier (eps >= 1e-11), and a period d
-// that is a power of two, so that scaling the points by 2 / d is exact. Host-only (the
-// work-item count of pwb_near_sym_items needs no device). PWB_NO_PROD=1: off (A/B, tests).
+// Product form of the symmetric Laplace and Stokeslet tiles (near_sym_impl.cuh SymLaplace /
+// SymStokes PROD): Laplace on a singly periodic cell (one image row of three), the Stokeslet
+// without pressure on an unskewed doubly periodic cell with 3 x 3 images; a reduced
+// precision tier (eps >= 1e-11); and a period d that is a power of two, so that scaling the
+// points by 2 / d is exact. Host-only (the work-item count of pwb_near_sym_items needs no
+// device). PWB_NO_PROD=1: off (A/B, tests).
 bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
-  if (nk != NearKind::Laplace || pz.cell.periodicity != periwave::Periodicity::Singly || n < 4096) return false;
-  if (!(pz.eps >= 1e-11) || std::getenv("PWB_FULL_PRECISION") != nullptr) return false;
+  const periwave::UnitCell& c = pz.cell;
+  if (nk == NearKind::Laplace) {
+    if (c.periodicity != periwave::Periodicity::Singly) return false;
+  } else if (nk == NearKind::Stokes) {
+    if (c.periodicity != periwave::Periodicity::Doubly || c.xi != 0.0 || c.m0 != 1 || pz.dlp) return false;
+  } else {
+    return false;
+  }
+  if (n < 4096 || !(pz.eps >= 1e-11) || std::getenv("PWB_FULL_PRECISION") != nullptr) return false;
   if (std::getenv("PWB_NO_PROD") != nullptr || std::getenv("PWB_NO_BINNING") != nullptr) return false;
   int e = 0;
-  const double d = pz.cell.d;
-  return d > 0.0 && std::frexp(d, &e) == 0.5 && e >= -400 && e <= 400;
+  return c.d > 0.0 && std::frexp(c.d, &e) == 0.5 && e >= -400 && e <= 400;
 }
 // Sets the tile's constants when eligible; the caller bins (bin_inputs scales the gathered points).
 bool prod_form(const periwave::Periodizer& pz, NearKind nk, NearArgs& a, size_t n) {
-  if (!prod_eligible(pz, nk, n) || !a.lowp || a.nxi != 3 || a.nrow != 1) return false;
+  if (!prod_eligible(pz, nk, n) || !a.lowp || a.nxi != 3) return false;
+  if (a.nrow != (nk == NearKind::Laplace ? 1 : 3)) return false;
   int e = 0;
   std::frexp(pz.cell.d, &e);
   a.prod_sc = std::ldexp(1.0, 2 - e);  // 2 / d
-  const double lnsc = static_cast<double>(2 - e) * 0.6931471805599453094;
-  a.prod_log_off = 4.0 * 0.6931471805599453094 - 6.0 * lnsc;  // ln(16 / sc^6)
+  const double ln2 = 0.6931471805599453094, lnsc = static_cast<double>(2 - e) * ln2;
+  // Laplace: the tile's product is (sc^6 / 16) P; Stokeslet: (sc^18 / 512) P
+  a.prod_log_off = nk == NearKind::Laplace ? 4.0 * ln2 - 6.0 * lnsc : 9.0 * ln2 - 18.0 * lnsc;
   a.prod_ln_sc2 = 2.0 * lnsc;
+  a.prod_eta = pz.cell.eta * a.prod_sc;
   return true;
 }
 

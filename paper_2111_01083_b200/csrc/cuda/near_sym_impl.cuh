@@ -200,7 +200,8 @@ struct SymLaplace {
   static_assert(!PROD || LOWP_, "the product form belongs to the reduced tiers");
   // product form of a separated tile pair (see above); dx, dy in the tile's units
   template <class LK, class B>
-  __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const LK& K, B& bad) {
+  __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const NearArgs&, const LK& K,
+                                                     B& bad) {
     const double U = dx * dx;
     const double W = fma(dy, dy, U);
     const double aa = fma(W, 0.25, 1.0);
@@ -278,7 +279,7 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool PROD = false, LOG_SEED = false;
   static constexpr int THREADS = 128;
   template <class LK, class B>
-  __device__ __forceinline__ static void values_prod(double*, double, double, const LK&, B&) {}  // SymLaplace only
+  __device__ __forceinline__ static void values_prod(double*, double, double, const NearArgs&, const LK&, B&) {}
   static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double*, double, double, const NearArgs&, const LK&, B&) {}
@@ -376,8 +377,16 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
 
 // Stokeslet: V = (log prod r2, Txx, Txy, Tyy [, Px, Py]) with T = sum r r^T / r^2,
 // P = sum r / r^2 (pressurelet, odd).
-template <bool PRESSURE, bool LOWP_, bool CLOG = false>  // CLOG: coarse table log (eps >= 1e-10)
+// PROD (no pressure, unskewed 3 x 3 images, binned points pre-scaled by a.prod_sc = 2 / d):
+// each image row in closed form. With U = dX^2, W = U + ry^2 (the middle image's r^2),
+// a = W / 4 + 1, b = a^2 - U (= r-^2 r+^2 / 16) the row's three images give
+//   sum 1/r^2  = (2 b + a W) / (2 W b),     sum rx/r^2 = dX (2 b + (a - 2) W) / (2 W b),
+// so one reciprocal (of 2 W b, which is also the row's factor of the log's product) serves
+// three images: 17 fp64 instructions per row where the image loop needs 22. The same
+// cancellation in b as the Laplace product form, the same per-tile-pair rule (prod_mode).
+template <bool PRESSURE, bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse table log (eps >= 1e-10)
 struct SymStokes {
+  static_assert(!PROD_ || (!PRESSURE && LOWP_), "the product form: velocity only, reduced tiers");
   // Without pressure the tile carries (a, Txy, b) with a = L/2 - Txx, b = L/2 - Tyy and
   // accumulates the two velocity components directly (u_x ~ a f_x - Txy f_y, u_y ~
   // b f_y - Txy f_x): 4 fp64 per side instead of 6 and half the column partials. With
@@ -387,10 +396,42 @@ struct SymStokes {
                                                                                                 : PWB_SYM_STOKES_TPT,
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
                        LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
-  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = false, LOG_SEED = false;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_, LOG_SEED = false;
   static constexpr int THREADS = 128;
   template <class LK, class B>
-  __device__ __forceinline__ static void values_prod(double*, double, double, const LK&, B&) {}  // SymLaplace only
+  __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const NearArgs& a, const LK& K,
+                                                     B& bad) {
+    if constexpr (PROD_) {
+      const double U = dx * dx;
+      double P = 1.0, tyy = 0.0, txyq = 0.0;
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        const double ry = n == 1 ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta);  // (dy) - shift, shift = (n - 1) eta
+        const double ry2 = ry * ry;
+        const double W = ry2 + U;
+        const double aa = fma(W, 0.25, 1.0);
+        const double b = fma(aa, aa, -U);
+        const double b2 = b + b;
+        const double Pr = W * b2;  // 2 W b = r0^2 r-^2 r+^2 / 8
+        const double inv = pwk::rcp_tier<LOWP>(Pr);
+        const double S = fma(aa, W, b2) * inv;        // sum_m 1 / r^2
+        const double Rq = fma(aa - 2.0, W, b2) * inv;  // sum_m rx / r^2, over dX
+        if (n == 0) {
+          P = Pr;
+          tyy = ry2 * S;
+          txyq = ry * Rq;
+        } else {
+          P *= Pr;
+          tyy = fma(ry2, S, tyy);
+          txyq = fma(ry, Rq, txyq);
+        }
+      }
+      const double L = pwk::log_fast(P, K, bad);  // the table carries ln(512 / sc^18)
+      V[0] = fma(0.5, L, tyy - 9.0);  // L/2 - Txx, Txx = 9 - Tyy
+      V[1] = dx * txyq;
+      V[2] = fma(0.5, L, -tyy);
+    }
+  }
   template <int NXI, int NROW, bool USK, class LK, class B>
   __device__ __forceinline__ static void values_fast(double* V, double dx, double dy, const NearArgs& a,
                                                      const LK& K, B& bad) {
@@ -398,15 +439,17 @@ struct SymStokes {
     //   Tyy = sum_n ry_n^2 S_n, Txx = images - Tyy (rx^2/r^2 + ry^2/r^2 = 1 per image; no
     //   exact zero on this path), Txy = sum_n ry_n R_n, pressurelet (sum_n R_n, sum_n ry_n S_n):
     // two fp64 instructions per image besides the reciprocal, instead of three.
-    double P = 1.0, tyy = 0.0, txy = 0.0, px = 0.0, py = 0.0;
+    // PROD (scaled points, period 2, rows at -eta, 0, eta in the tile's units): the product
+    // is sc^18 P, the table expects P / 512 of it
+    double P = PROD_ ? 0x1p-9 : 1.0, tyy = 0.0, txy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
+      const double ry = PROD_ ? (n == 1 ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta)) : row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
       double S = 0.0, R = 0.0;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW, USK>(dx, a, n, m);
+        const double rx = PROD_ ? (m == 1 ? dx : dx - 2.0 * (m - 1)) : img_dx<NXI, NROW, USK>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
         const double inv = pwk::rcp_tier<LOWP>(r2);
@@ -449,14 +492,17 @@ struct SymStokes {
     double L = 0.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
     for (int n = 0; n < NROW; ++n)
       for (int m = 0; m < NXI; ++m) {
-        const double rx = img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = row_dy<NXI, NROW>(dy, a, n);
+        // PROD: scaled points (shifts 2 (m - 1), (n - 1) eta in the tile's units); the tensor
+        // terms do not depend on the scale, each image's log carries ln sc^2
+        const double rx = PROD_ ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = PROD_ ? dy - a.prod_eta * (n - 1) : row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
         }
         const double r2 = fma(rx, rx, ry * ry);
         L += pwk::log_r2_safe(rx, ry);
+        if (PROD_) L -= a.prod_ln_sc2;
         txx += rx * rx / r2;
         txy += rx * ry / r2;
         tyy += ry * ry / r2;
@@ -555,23 +601,30 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
   return mask;
 }
 
-// Product-form Laplace tile (SymLaplace PROD), per tile pair from the row box and the column
-// box (xmin, -xmax, ymin, -ymax; the period is 2 in the tile's units):
-//   0  some pair may come within a quarter unit (d / 8) of the +2 or the -2 image in both x
-//      and y: the image loop;
-//   1  every pair stays clear of both images: the product form;
-//   2  and the boxes themselves are apart (by more than 2^-100), so no pair coincides and
-//      every product is a normal number: the product form without the exponent check and
-//      without the saved row sums of the careful redo (9 registers the loop can use).
-__device__ __forceinline__ int prod_mode(const double* tb, const double* sb) {
+// Product-form tiles (SymLaplace / SymStokes PROD), per tile pair from the row box and the
+// column box (xmin, -xmax, ymin, -ymax; the period is 2 in the tile's units, the image rows
+// sit at (n - 1) eta):
+//   0  some pair may come within a quarter unit (d / 8) of an image of the +2 or the -2
+//      column in both x and y: the image loop;
+//   1  every pair stays clear of those images: the product form;
+//   2  and no image can coincide with a pair at all (the boxes are apart by more than
+//      2^-100 around every image), so every product is a normal number: the product form
+//      without the exponent check and without the saved row sums of the careful redo.
+template <int NROW>
+__device__ __forceinline__ int prod_mode(const double* tb, const double* sb, double eta) {
   const double xlo = tb[0] + sb[1], xhi = -tb[1] - sb[0];  // range of t.x - s.x
   const double ylo = tb[2] + sb[3], yhi = -tb[3] - sb[2];
-  const double gy = ylo > 0.0 ? ylo : (yhi < 0.0 ? -yhi : 0.0);
-  const double gx = xlo > 0.0 ? xlo : (xhi < 0.0 ? -xhi : 0.0);
-  const double gp = xlo > 2.0 ? xlo - 2.0 : (xhi < 2.0 ? 2.0 - xhi : 0.0);    // gap to +2
-  const double gm = xlo > -2.0 ? xlo + 2.0 : (xhi < -2.0 ? -2.0 - xhi : 0.0);  // gap to -2
-  if (!(fmax(fmin(gp, gm), gy) >= 0.25)) return 0;
-  return fmax(gx, gy) > 0x1p-100 ? 2 : 1;
+  auto gap = [](double lo, double hi, double c) { return lo > c ? lo - c : (hi < c ? c - hi : 0.0); };
+  const double gx0 = gap(xlo, xhi, 0.0);
+  const double gxs = fmin(gap(xlo, xhi, 2.0), gap(xlo, xhi, -2.0));  // to the nearer side column
+  int mode = 2;
+#pragma unroll
+  for (int n = 0; n < NROW; ++n) {
+    const double gy = gap(ylo, yhi, NROW == 1 ? 0.0 : (n - 1) * eta);
+    if (!(fmax(gxs, gy) >= 0.25)) return 0;
+    if (!(fmax(gx0, gy) > 0x1p-100)) mode = 1;
+  }
+  return mode;
 }
 
 template <class K, int NXI, int NROW, bool USK>
@@ -831,7 +884,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
           double V[K::NV];
           // (t - s) - shift as upstream (apply.cpp:534)
           if constexpr (decltype(prod)::value)
-            K::values_prod(V, tx[k] - sx, ty[k] - sy, LK, bad);
+            K::values_prod(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
           else
             K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
           K::row(racc[k], V, w);
@@ -844,7 +897,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     using BadT = std::conditional_t<kTab, unsigned, int>;  // see pwk::log_bad
     int pmode = 0;
     if constexpr (K::PROD) {
-      pmode = prod_mode(rb, cbx);  // block-uniform
+      pmode = prod_mode<NROW>(rb, cbx, a.prod_eta);  // block-uniform
       // dead rows / columns sit at the origin with weight 0: their products may vanish, so a
       // ragged tile pair keeps the check
       if (pmode == 2 && (static_cast<size_t>(I + 1) * TILE > n || jbase + CT > n)) pmode = 1;

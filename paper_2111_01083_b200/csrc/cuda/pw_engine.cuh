@@ -88,12 +88,13 @@ struct NearArgs {
   int coarse_log = 0;            // symmetric Laplace / Stokeslet tiles: 256-entry table log (eps >= 1e-10)
   double cheb_tol = 0.0;         // screened symmetric tile: per-tile-pair Chebyshev K0 fit (0: off)
   double inv_beta2 = 0.0;
-  // Product-form symmetric Laplace tile (one image row, near_sym_impl.cuh SymLaplace PROD):
+  // Product-form symmetric tiles (near_sym_impl.cuh SymLaplace / SymStokes PROD):
   // src / tgt hold the binned points times prod_sc = 2 / d, an exact power of two (0: off),
   // so the period is 2 in the tile's units
   double prod_sc = 0.0;
-  double prod_log_off = 0.0;     // ln(16 / prod_sc^6): added to the log table's entries
+  double prod_log_off = 0.0;     // ln(16 / prod_sc^6) (Laplace), ln(512 / prod_sc^18) (Stokeslet): added to the log table's entries
   double prod_ln_sc2 = 0.0;      // ln(prod_sc^2): one image's log offset on the careful path
+  double prod_eta = 0.0;         // eta * prod_sc: the image rows' offset in the tile's units (3 x 3 images)
   // host side only: a split one-sided tile may run on its own stream (a parallel branch of a
   // captured small call, engine.cu total_eager); the partials' reduction waits for tile_done
   void* tile_stream = nullptr;
