@@ -1111,20 +1111,16 @@ void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, 
 }
 
 // Product form of the symmetric Laplace and Stokeslet tiles (near_sym_impl.cuh SymLaplace /
-// SymStokes PROD): Laplace on a singly periodic cell (one image row of three), the Stokeslet
-// without pressure on an unskewed doubly periodic cell with 3 x 3 images; a reduced
+// SymStokes PROD): Laplace on a singly periodic cell (one image row of three) or an unskewed
+// doubly periodic one with 3 x 3 images, the Stokeslet without pressure on the latter; a reduced
 // precision tier (eps >= 1e-11); and a period d that is a power of two, so that scaling the
 // points by 2 / d is exact. Host-only (the work-item count of pwb_near_sym_items needs no
 // device). PWB_NO_PROD=1: off (A/B, tests).
 bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
   const periwave::UnitCell& c = pz.cell;
-  if (nk == NearKind::Laplace) {
-    if (c.periodicity != periwave::Periodicity::Singly) return false;
-  } else if (nk == NearKind::Stokes) {
-    if (c.periodicity != periwave::Periodicity::Doubly || c.xi != 0.0 || c.m0 != 1 || pz.dlp) return false;
-  } else {
-    return false;
-  }
+  if (nk != NearKind::Laplace && nk != NearKind::Stokes) return false;
+  if (nk == NearKind::Stokes && (c.periodicity != periwave::Periodicity::Doubly || pz.dlp)) return false;
+  if (c.periodicity == periwave::Periodicity::Doubly && (c.xi != 0.0 || c.m0 != 1)) return false;
   if (n < 4096 || !(pz.eps >= 1e-11) || std::getenv("PWB_FULL_PRECISION") != nullptr) return false;
   if (std::getenv("PWB_NO_PROD") != nullptr || std::getenv("PWB_NO_BINNING") != nullptr) return false;
   int e = 0;
@@ -1133,13 +1129,13 @@ bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
 // Sets the tile's constants when eligible; the caller bins (bin_inputs scales the gathered points).
 bool prod_form(const periwave::Periodizer& pz, NearKind nk, NearArgs& a, size_t n) {
   if (!prod_eligible(pz, nk, n) || !a.lowp || a.nxi != 3) return false;
-  if (a.nrow != (nk == NearKind::Laplace ? 1 : 3)) return false;
+  if (a.nrow != (pz.cell.periodicity == periwave::Periodicity::Singly ? 1 : 3)) return false;
   int e = 0;
   std::frexp(pz.cell.d, &e);
   a.prod_sc = std::ldexp(1.0, 2 - e);  // 2 / d
   const double ln2 = 0.6931471805599453094, lnsc = static_cast<double>(2 - e) * ln2;
-  // Laplace: the tile's product is (sc^6 / 16) P; Stokeslet: (sc^18 / 512) P
-  a.prod_log_off = nk == NearKind::Laplace ? 4.0 * ln2 - 6.0 * lnsc : 9.0 * ln2 - 18.0 * lnsc;
+  // Laplace: the tile's product is (sc^6 / 16) P per image row; Stokeslet: (sc^18 / 512) P
+  a.prod_log_off = nk == NearKind::Laplace ? a.nrow * (4.0 * ln2 - 6.0 * lnsc) : 9.0 * ln2 - 18.0 * lnsc;
   a.prod_ln_sc2 = 2.0 * lnsc;
   a.prod_eta = pz.cell.eta * a.prod_sc;
   return true;

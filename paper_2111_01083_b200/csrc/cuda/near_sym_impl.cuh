@@ -92,6 +92,9 @@ namespace sym {
 #ifndef PWB_SYM_STOKES_CPT
 #define PWB_SYM_STOKES_CPT 2  // column points per thread of the Stokeslet tile
 #endif
+#ifndef PWB_SYM_STOKES_UNROLL
+#define PWB_SYM_STOKES_UNROLL 2  // sources per unrolled step of the Stokeslet tile's fast loop
+#endif
 #ifndef PWB_SYM_STOKES_MINB
 #define PWB_SYM_STOKES_MINB 0  // 0: ptxas's own register allocation (166 registers, 3 blocks/SM)
 #endif
@@ -192,21 +195,26 @@ struct SymLaplace {
                        MINB = PROD_ ? PWB_SYM_PROD_MINB : PWB_SYM_LAPLACE_MINB,
                        UNROLL = PROD_ ? PWB_SYM_PROD_UNROLL : PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_;
-  // PROD: 256 threads share one conflict-free 8-replica table (32 KB at 256 entries): the
-  // tile is bound by shared-memory wavefronts next to the fp64 pipe (ncu r2s: 86 % / 68 %),
-  // and the 4-replica table's bank conflicts cost 2.4 of its 9.2 wavefronts per warp and pair
   static constexpr int THREADS = PROD_ ? PWB_SYM_PROD_THREADS : 128;
   static constexpr bool LOG_SEED = PROD_ && PWB_SYM_PROD_SEED;  // table type: pwk::LogR instead of pwk::LogT
   static_assert(!PROD || LOWP_, "the product form belongs to the reduced tiers");
-  // product form of a separated tile pair (see above); dx, dy in the tile's units
-  template <class LK, class B>
-  __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const NearArgs&, const LK& K,
+  // product form of a separated tile pair (see above); dx, dy in the tile's units. NROW == 3
+  // (unskewed doubly periodic cells): every image row at (n - 1) eta has the same closed
+  // form with its own ry; 19 fp64 instructions for the 9 images where the image loop needs 26.
+  template <int NROW, class LK, class B>
+  __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const NearArgs& a, const LK& K,
                                                      B& bad) {
     const double U = dx * dx;
-    const double W = fma(dy, dy, U);
-    const double aa = fma(W, 0.25, 1.0);
-    const double b = fma(aa, aa, -U);
-    V[0] = pwk::log_fast(W * b, K, bad);
+    double P = 1.0;
+#pragma unroll
+    for (int n = 0; n < NROW; ++n) {
+      const double ry = (NROW == 1 || n == 1) ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta);
+      const double W = fma(ry, ry, U);
+      const double aa = fma(W, 0.25, 1.0);
+      const double b = fma(aa, aa, -U);
+      P = n == 0 ? W * b : P * (W * b);
+    }
+    V[0] = pwk::log_fast(P, K, bad);
   }
   // 128-point column tiles under the 512-point row tile: the staged sources and per-warp
   // column partials take 7 KB, so the conflict-free 8-replica log table (16 KB) and 7
@@ -219,14 +227,18 @@ struct SymLaplace {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = row_dy<NXI, NROW>(dy, a, n);
+      const double ry = !PROD ? row_dy<NXI, NROW>(dy, a, n)
+                              : ((NROW == 1 || n == 1) ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta));
       ry2[n] = ry * ry;
     }
     if constexpr (PROD) {
-      // scaled points: shifts -2, 0, 2; the product is sc^6 P = 16 P', the table expects P'
-      static_assert(!PROD || (NXI == 3 && NROW == 1), "one image row of three");
+      // scaled points: column shifts -2, 0, 2, rows at (n - 1) eta; per row the product is
+      // sc^6 P_row = 16 P'_row, the table expects P'
+      static_assert(!PROD || (NXI == 3 && (NROW == 1 || NROW == 3)), "image rows of three");
       const double xm = dx + 2.0, xp = dx - 2.0;
-      const double P = (fma(xm, xm, ry2[0]) * 0x1p-4) * (fma(dx, dx, ry2[0]) * fma(xp, xp, ry2[0]));
+      double P = NROW == 1 ? 0x1p-4 : 0x1p-12;
+#pragma unroll
+      for (int n = 0; n < NROW; ++n) P *= fma(xm, xm, ry2[n]) * (fma(dx, dx, ry2[n]) * fma(xp, xp, ry2[n]));
       V[0] = pwk::log_fast(P, K, bad);
       return;
     }
@@ -247,7 +259,7 @@ struct SymLaplace {
       for (int m = 0; m < NXI; ++m) {
         // PROD: scaled points, shift m d * sc = 2 (m - 1); each image's log carries ln sc^2
         const double rx = PROD ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = PROD ? dy : row_dy<NXI, NROW>(dy, a, n);
+        const double ry = PROD ? (NROW == 1 ? dy : dy - a.prod_eta * (n - 1)) : row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
@@ -278,7 +290,7 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
   static constexpr bool CHEB = !GRAD;     // regime 3: per-tile-pair Chebyshev K0 (pw_math.cuh cheb_fit_k0)
   static constexpr bool PROD = false, LOG_SEED = false;
   static constexpr int THREADS = 128;
-  template <class LK, class B>
+  template <int NROW, class LK, class B>
   __device__ __forceinline__ static void values_prod(double*, double, double, const NearArgs&, const LK&, B&) {}
   static constexpr int CPT = TPT, LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = pwk::kLogTabBits;
   template <int NXI, int NROW, bool USK, class LK, class B>
@@ -394,11 +406,11 @@ struct SymStokes {
   static constexpr int NW = 2, NV = PRESSURE ? 6 : 3, NACC = PRESSURE ? 5 : 2, NOUT = PRESSURE ? 3 : 2,
                        TPT = PWB_SYM_STOKES_TPT, CPT = PWB_SYM_STOKES_CPT < PWB_SYM_STOKES_TPT ? PWB_SYM_STOKES_CPT
                                                                                                 : PWB_SYM_STOKES_TPT,
-                       CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = 2,
+                       CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = PWB_SYM_STOKES_UNROLL,
                        LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_, LOG_SEED = false;
   static constexpr int THREADS = 128;
-  template <class LK, class B>
+  template <int NROW, class LK, class B>
   __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const NearArgs& a, const LK& K,
                                                      B& bad) {
     if constexpr (PROD_) {
@@ -884,7 +896,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
           double V[K::NV];
           // (t - s) - shift as upstream (apply.cpp:534)
           if constexpr (decltype(prod)::value)
-            K::values_prod(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
+            K::template values_prod<NROW>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
           else
             K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, bad);
           K::row(racc[k], V, w);

@@ -203,3 +203,69 @@ def test_stokeslet_product_form_duplicates_and_image_coincidence(pw, gpu):
         with pytest.raises(pw.PeriwaveError) as e:
             pw.near_field(pz, pw.ParticleSystem(sources=bad, targets=bad, forces=f))
         assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
+
+
+# ------------------------------------------------------------------ Laplace, 3 x 3 images
+@pytest.mark.parametrize("eps", [1e-10, 1e-11])
+@pytest.mark.parametrize("d,eta", [(1.0, 1.0), (2.0, 0.7), (0.5, 0.4)])
+def test_laplace_3x3_product_form_matches_image_loop(pw, gpu, ref, monkeypatch, d, eta, eps):
+    """Unskewed doubly periodic Poisson above the symmetric threshold: every image row in
+    closed form."""
+    rng = np.random.default_rng(int(d * 8) + 41)
+    n = 36000
+    src = _points2(rng, d, eta, n)
+    q = rng.standard_normal(n)
+    q -= q.mean()
+    cell = pw.make_unit_cell(d, 0.0, eta)
+    if cell.m0 != 1:
+        pytest.skip("more than 3 x 3 images")
+    pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, eps)
+    sys_ = pw.ParticleSystem(sources=src, targets=src, charges=q)
+    prod = pw.near_field(pz, sys_).scalar
+    assert np.array_equal(prod, pw.near_field(pz, sys_).scalar)
+    monkeypatch.setenv("PWB_NO_PROD", "1")
+    loop = pw.near_field(pz, sys_).scalar
+    monkeypatch.delenv("PWB_NO_PROD")
+    assert not np.array_equal(prod, loop)
+    monkeypatch.setenv("PWB_FULL_PRECISION", "1")
+    full = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), charges=q)).scalar
+    monkeypatch.delenv("PWB_FULL_PRECISION")
+    e_prod, e_loop = rel_l2(prod, full), rel_l2(loop, full)
+    print("d", d, "eta", eta, "eps", eps, "prod vs full", e_prod, "image loop vs full", e_loop)
+    assert e_prod <= (2e-12 if eps >= 1e-10 else 5e-13)
+    assert e_prod <= 2.0 * e_loop + 1e-13
+    idx = rng.choice(n, 200, replace=False)
+    tg = np.ascontiguousarray(src[idx])
+    R = ref.make_periodizer(int(pw.Pde.Poisson), 0.0, (d, 0.0, eta, int(pw.Periodicity.Doubly)), eps)
+    want = R.apply(2, src, tg, charges=q, threads=8)["scalar"]
+    assert rel_l2(prod[idx], want) <= 1e-11
+
+
+def test_laplace_3x3_product_form_duplicates_and_image_coincidence(pw, gpu, monkeypatch):
+    rng = np.random.default_rng(43)
+    n = 36000
+    src = _points2(rng, 1.0, 1.0, n)
+    src[1000:1010] = src[30000:30010]
+    src[5] = src[6]
+    q = rng.standard_normal(n)
+    q -= q.mean()
+    pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, pw.make_unit_cell(1.0, 0.0, 1.0), 1e-10)
+    sym = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src, charges=q)).scalar
+    one = pw.near_field(pz, pw.ParticleSystem(sources=src, targets=src.copy(), charges=q)).scalar
+    assert np.all(np.isfinite(sym))
+    assert rel_l2(sym, one) <= 2e-12
+    for p7, p3 in [([-0.5, 0.25], [0.5, 0.25]), ([0.3, -0.5], [0.3, 0.5]), ([-0.5, 0.5], [0.5, -0.5])]:
+        bad = src.copy()
+        bad[7] = p7
+        bad[33333] = p3
+        with pytest.raises(pw.PeriwaveError) as e:
+            pw.near_field(pz, pw.ParticleSystem(sources=bad, targets=bad, charges=q))
+        assert e.value.code == pw.ErrorCode.CoincidentSourceTarget
+    # a skewed cell keeps the image loop
+    sk = pw.make_periodizer(pw.Pde.Poisson, 0.0, pw.make_unit_cell(1.0, 0.25, 0.9), 1e-10)
+    pts = np.ascontiguousarray(np.column_stack([rng.uniform(-0.5, 0.5, n), rng.uniform(-0.5, 0.5, n)])
+                               @ np.array([[1.0, 0.0], [0.25, 0.9]]))
+    a = pw.near_field(sk, pw.ParticleSystem(sources=pts, targets=pts, charges=q)).scalar
+    monkeypatch.setenv("PWB_NO_PROD", "1")
+    b = pw.near_field(sk, pw.ParticleSystem(sources=pts, targets=pts, charges=q)).scalar
+    assert np.array_equal(a, b)
