@@ -123,6 +123,9 @@ namespace sym {
 #ifndef PWB_SYM_PROD_UNROLL
 #define PWB_SYM_PROD_UNROLL 2
 #endif
+#ifndef PWB_SYM_PROD_ITEM_SOURCES
+#define PWB_SYM_PROD_ITEM_SOURCES 1024  // sources per work item: 0.66 ms items, so an 8-rank split's last wave costs ~1 % (4096: 2.7 ms items, 8-rank near efficiency 0.93, r3p)
+#endif
 #ifndef PWB_SYM_PROD_THREADS
 #define PWB_SYM_PROD_THREADS 128  // threads per block (A/B r2w: 256 with one 8-replica table per 8 warps 608 ms vs 572)
 #endif
@@ -191,7 +194,8 @@ template <bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse ta
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PROD_ ? PWB_SYM_PROD_TPT : PWB_SYM_LAPLACE_TPT,
                        CPT = PROD_ ? PWB_SYM_PROD_CPT : PWB_SYM_LAPLACE_CPT,
-                       CHUNK = PROD_ ? 32 / PWB_SYM_PROD_CPT : 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
+                       CHUNK = PROD_ ? PWB_SYM_PROD_ITEM_SOURCES / (128 * PWB_SYM_PROD_CPT)
+                                     : 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
                        MINB = PROD_ ? PWB_SYM_PROD_MINB : PWB_SYM_LAPLACE_MINB,
                        UNROLL = PROD_ ? PWB_SYM_PROD_UNROLL : PWB_SYM_LAPLACE_UNROLL;
   static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_;
@@ -772,7 +776,63 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
       mask = image_mask<NXI, NROW>(rb, cbx, a);
       if (mask == 0u) continue;  // block-uniform: no pair of this tile pair is in range
     }
-    if (J < (I + 1) * R) {  // inside the row tile: one-sided and careful (self pairs live here)
+    if (J < (I + 1) * R) {  // inside the row tile: one-sided (self pairs live here)
+      if constexpr (K::FAST) {
+        // Fast one-sided sweep: every ordered pair once with the branch-free pair values; a
+        // thread's own point (identity image skipped, apply.cpp:538-545) takes the other
+        // images' values at the pure shifts, which the careful evaluation of a zero delta
+        // returns (once per tile). A duplicate point or an image coincidence makes a product
+        // vanish and sends the tile to the careful sweep below. The careful sweep alone is
+        // ~10x slower per pair: these tiles are ~0.1 % of the pairs, but one such work item
+        // per row tile ran 5-7 ms and sat at the end of every rank's item range (8-rank near
+        // efficiency of c4 0.93, r3p).
+        double Vself[K::NV];
+        {
+          int f0 = 0;
+          call_values<K, NXI, NROW>(Vself, 0.0, 0.0, a, f0, mask);
+        }
+        double keepd[TPT][K::NACC];
+#pragma unroll
+        for (int k = 0; k < TPT; ++k)
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c) keepd[k][c] = racc[k][c];
+        using BadD = std::conditional_t<kTab, unsigned, int>;
+        BadD badd = 0;
+        const bool dprod = K::PROD && prod_mode<NROW>(rb, cbx, a.prod_eta) >= 1;  // block-uniform
+        const size_t l0 = static_cast<size_t>(I) * TILE + tid;
+        auto diag_loop = [&](auto prod) {
+#pragma unroll 2
+          for (int i = 0; i < CT; ++i) {
+            const double sx = s_x[i], sy = s_y[i];
+            double w[K::NW];
+#pragma unroll
+            for (int c = 0; c < K::NW; ++c) w[c] = s_w[c][i];
+#pragma unroll
+            for (int k = 0; k < TPT; ++k) {
+              double V[K::NV];
+              BadD b1 = 0;
+              if constexpr (decltype(prod)::value)
+                K::template values_prod<NROW>(V, tx[k] - sx, ty[k] - sy, a, LK, b1);
+              else
+                K::template values_fast<NXI, NROW, USK>(V, tx[k] - sx, ty[k] - sy, a, LK, b1);
+              const bool self = jbase + i == l0 + static_cast<size_t>(k) * kT;
+              if (!self) badd = max(badd, b1);
+#pragma unroll
+              for (int c = 0; c < K::NV; ++c) V[c] = self ? Vself[c] : V[c];
+              K::row(racc[k], V, w);
+            }
+          }
+        };
+        if (dprod)
+          diag_loop(std::true_type{});
+        else
+          diag_loop(std::false_type{});
+        if (!__syncthreads_or(pwk::log_bad(LK, badd))) continue;
+#pragma unroll
+        for (int k = 0; k < TPT; ++k)
+#pragma unroll
+          for (int c = 0; c < K::NACC; ++c) racc[k][c] = keepd[k][c];
+      }
       for (int i = 0; i < CT; ++i) {
         const double sx = s_x[i], sy = s_y[i];
         double w[K::NW];

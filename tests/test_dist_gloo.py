@@ -232,8 +232,8 @@ def test_item_counts_match_the_device_decomposition(pw):
             nb, ncb, r, chunk = (n + 511) // 512, (n + 127) // 128, 4, 32
         else:
             # product-form tile (singly periodic, d a power of two, binned from 4096 points):
-            # 1024-point row tiles (8 targets x 128 threads), 256-point column tiles, 16 per item
-            nb, ncb, r, chunk = (n + 1023) // 1024, (n + 255) // 256, 4, 16
+            # 1024-point row tiles (8 targets x 128 threads), 256-point column tiles, 4 per item
+            nb, ncb, r, chunk = (n + 1023) // 1024, (n + 255) // 256, 4, 4
         assert items == sum((ncb - r * i + chunk - 1) // chunk for i in range(nb))
         assert nout == 1
         if want is not None:
