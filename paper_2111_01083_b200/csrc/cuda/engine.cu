@@ -1112,10 +1112,9 @@ void Plan::fixed_finish(const Opts& o, const unsigned long long* acc, size_t n, 
 
 // Product form of the symmetric Laplace and Stokeslet tiles (near_sym_impl.cuh SymLaplace /
 // SymStokes PROD): Laplace on a singly periodic cell (one image row of three) or an unskewed
-// doubly periodic one with 3 x 3 images, the Stokeslet without pressure on the latter; a reduced
-// precision tier (eps >= 1e-11); and a period d that is a power of two, so that scaling the
-// points by 2 / d is exact. Host-only (the work-item count of pwb_near_sym_items needs no
-// device). PWB_NO_PROD=1: off (A/B, tests).
+// doubly periodic one with 3 x 3 images, the Stokeslet without pressure on the latter; a
+// reduced precision tier (eps >= 1e-11). Host-only (the work-item count of
+// pwb_near_sym_items needs no device). PWB_NO_PROD=1: off (A/B, tests).
 bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
   const periwave::UnitCell& c = pz.cell;
   if (nk != NearKind::Laplace && nk != NearKind::Stokes) return false;
@@ -1123,20 +1122,33 @@ bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
   if (c.periodicity == periwave::Periodicity::Doubly && (c.xi != 0.0 || c.m0 != 1)) return false;
   if (n < 4096 || !(pz.eps >= 1e-11) || std::getenv("PWB_FULL_PRECISION") != nullptr) return false;
   if (std::getenv("PWB_NO_PROD") != nullptr || std::getenv("PWB_NO_BINNING") != nullptr) return false;
-  int e = 0;
-  return c.d > 0.0 && std::frexp(c.d, &e) == 0.5 && e >= -400 && e <= 400;
+  return c.d > 0.0 && c.d >= 0x1p-400 && c.d <= 0x1p400;
 }
-// Sets the tile's constants when eligible; the caller bins (bin_inputs scales the gathered points).
+// Sets the tile's constants when eligible; the caller bins (bin_inputs scales the gathered
+// points). A period that is a power of two lets the points be scaled by 2 / d exactly (the
+// cheaper form, prod = 1); any other period keeps them unscaled (prod = 2).
 bool prod_form(const periwave::Periodizer& pz, NearKind nk, NearArgs& a, size_t n) {
   if (!prod_eligible(pz, nk, n) || !a.lowp || a.nxi != 3) return false;
   if (a.nrow != (pz.cell.periodicity == periwave::Periodicity::Singly ? 1 : 3)) return false;
+  const double d = pz.cell.d;
   int e = 0;
-  std::frexp(pz.cell.d, &e);
-  a.prod_sc = std::ldexp(1.0, 2 - e);  // 2 / d
-  const double ln2 = 0.6931471805599453094, lnsc = static_cast<double>(2 - e) * ln2;
-  // Laplace: the tile's product is (sc^6 / 16) P per image row; Stokeslet: (sc^18 / 512) P
-  a.prod_log_off = nk == NearKind::Laplace ? a.nrow * (4.0 * ln2 - 6.0 * lnsc) : 9.0 * ln2 - 18.0 * lnsc;
-  a.prod_ln_sc2 = 2.0 * lnsc;
+  if (std::frexp(d, &e) == 0.5 && std::getenv("PWB_PROD_UNSCALED") == nullptr) {
+    a.prod = 1;
+    a.prod_sc = std::ldexp(1.0, 2 - e);  // 2 / d
+    a.prod_period = 2.0;
+    const double ln2 = 0.6931471805599453094, lnsc = static_cast<double>(2 - e) * ln2;
+    // Laplace: the tile's product is (sc^6 / 16) P per image row; Stokeslet: (sc^18 / 512) P
+    a.prod_log_off = nk == NearKind::Laplace ? a.nrow * (4.0 * ln2 - 6.0 * lnsc) : 9.0 * ln2 - 18.0 * lnsc;
+    a.prod_ln_sc2 = 2.0 * lnsc;
+  } else {
+    a.prod = 2;
+    a.prod_sc = 1.0;
+    a.prod_period = d;
+    a.prod_d2 = d * d;
+    a.prod_4d2 = 4.0 * (d * d);
+    a.prod_log_off = 0.0;
+    a.prod_ln_sc2 = 0.0;
+  }
   a.prod_eta = pz.cell.eta * a.prod_sc;
   return true;
 }
@@ -1161,7 +1173,7 @@ void Plan::bin_inputs(const DevSys& s, NearArgs& a, cudaStream_t st) {
   int* ps = bin_perm_s_.as<int>(s.ns);
   morton_order(a.src, s.ns, box, ps, ws, ws_bytes, st);
   double2* src = bin_src_.as<double2>(s.ns);
-  if (a.prod_sc != 0.0)
+  if (a.prod == 1)
     gather_scale_double2(a.src, ps, s.ns, a.prod_sc, src, st);
   else
     gather_double2(a.src, ps, s.ns, src, st);
@@ -1187,7 +1199,7 @@ void Plan::bin_inputs(const DevSys& s, NearArgs& a, cudaStream_t st) {
     int* pt = bin_perm_t_.as<int>(s.nt);
     morton_order(a.tgt, s.nt, box, pt, ws, ws_bytes, st);
     double2* tgt = bin_tgt_.as<double2>(s.nt);
-    if (a.prod_sc != 0.0)
+    if (a.prod == 1)
       gather_scale_double2(a.tgt, pt, s.nt, a.prod_sc, tgt, st);
     else
       gather_double2(a.tgt, pt, s.nt, tgt, st);

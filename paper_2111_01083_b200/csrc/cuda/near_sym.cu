@@ -261,7 +261,7 @@ void near_sym_split(NearKind kind, const NearArgs& a, int world, long* bounds_ho
 long near_sym_item_count(NearKind kind, size_t n, bool prod) {
   switch (kind) {
     case NearKind::Laplace:  // the product-form tile has its own row tile (near_sym_impl.cuh)
-      return prod ? item_count<sym::SymLaplace<true, true, true>>(n) : item_count<sym::SymLaplace<false>>(n);
+      return prod ? item_count<sym::SymLaplace<true, true, 1>>(n) : item_count<sym::SymLaplace<false>>(n);
     case NearKind::ModHelm: return item_count<sym::SymModHelm<false, false>>(n);
     case NearKind::ModHelmGrad: return item_count<sym::SymModHelm<true, false>>(n);
     case NearKind::Stokes: return item_count<sym::SymStokes<false, false>>(n);

@@ -190,7 +190,10 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double v, const Ne
 // is 3e-13): prod_mode(). Every other tile pair runs the image loop on the same scaled
 // points -- (t - s) - shift scales exactly by a power of two, so its values and its exact
 // zeros are those of the unscaled points (apply.cpp:534).
-template <bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse table log (eps >= 1e-10, a.coarse_log)
+// PROD_ = 1: as above. PROD_ = 2 (any other period): the same on the unscaled binned points,
+// with a = W + d^2 and b = a^2 - 4 d^2 U (one more multiplication per image row) and the
+// cell's own shifts in the image loop.
+template <bool LOWP_, bool CLOG = false, int PROD_ = 0>  // CLOG: coarse table log (eps >= 1e-10, a.coarse_log)
 struct SymLaplace {
   static constexpr int NW = 1, NV = 1, NACC = 1, NOUT = 1, TPT = PROD_ ? PWB_SYM_PROD_TPT : PWB_SYM_LAPLACE_TPT,
                        CPT = PROD_ ? PWB_SYM_PROD_CPT : PWB_SYM_LAPLACE_CPT,
@@ -198,7 +201,8 @@ struct SymLaplace {
                                      : 8 * PWB_SYM_LAPLACE_TPT / PWB_SYM_LAPLACE_CPT,  // 4096 sources per item
                        MINB = PROD_ ? PWB_SYM_PROD_MINB : PWB_SYM_LAPLACE_MINB,
                        UNROLL = PROD_ ? PWB_SYM_PROD_UNROLL : PWB_SYM_LAPLACE_UNROLL;
-  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_ != 0,
+                        SCALED = PROD_ == 1;  // points pre-scaled to period 2
   static constexpr int THREADS = PROD_ ? PWB_SYM_PROD_THREADS : 128;
   static constexpr bool LOG_SEED = PROD_ && PWB_SYM_PROD_SEED;  // table type: pwk::LogR instead of pwk::LogT
   static_assert(!PROD || LOWP_, "the product form belongs to the reduced tiers");
@@ -214,8 +218,8 @@ struct SymLaplace {
     for (int n = 0; n < NROW; ++n) {
       const double ry = (NROW == 1 || n == 1) ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta);
       const double W = fma(ry, ry, U);
-      const double aa = fma(W, 0.25, 1.0);
-      const double b = fma(aa, aa, -U);
+      const double aa = SCALED ? fma(W, 0.25, 1.0) : W + a.prod_d2;
+      const double b = SCALED ? fma(aa, aa, -U) : fma(aa, aa, -(a.prod_4d2 * U));
       P = n == 0 ? W * b : P * (W * b);
     }
     V[0] = pwk::log_fast(P, K, bad);
@@ -231,14 +235,14 @@ struct SymLaplace {
     double ry2[NROW];
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = !PROD ? row_dy<NXI, NROW>(dy, a, n)
-                              : ((NROW == 1 || n == 1) ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta));
+      const double ry = !SCALED ? row_dy<NXI, NROW>(dy, a, n)
+                                : ((NROW == 1 || n == 1) ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta));
       ry2[n] = ry * ry;
     }
-    if constexpr (PROD) {
+    if constexpr (SCALED) {
       // scaled points: column shifts -2, 0, 2, rows at (n - 1) eta; per row the product is
       // sc^6 P_row = 16 P'_row, the table expects P'
-      static_assert(!PROD || (NXI == 3 && (NROW == 1 || NROW == 3)), "image rows of three");
+      static_assert(!SCALED || (NXI == 3 && (NROW == 1 || NROW == 3)), "image rows of three");
       const double xm = dx + 2.0, xp = dx - 2.0;
       double P = NROW == 1 ? 0x1p-4 : 0x1p-12;
 #pragma unroll
@@ -261,15 +265,15 @@ struct SymLaplace {
     double L = 0.0;
     for (int n = 0; n < NROW; ++n)
       for (int m = 0; m < NXI; ++m) {
-        // PROD: scaled points, shift m d * sc = 2 (m - 1); each image's log carries ln sc^2
-        const double rx = PROD ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = PROD ? (NROW == 1 ? dy : dy - a.prod_eta * (n - 1)) : row_dy<NXI, NROW>(dy, a, n);
+        // SCALED: scaled points, shift m d * sc = 2 (m - 1); each image's log carries ln sc^2
+        const double rx = SCALED ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = SCALED ? (NROW == 1 ? dy : dy - a.prod_eta * (n - 1)) : row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
         }
         L += pwk::log_r2_safe(rx, ry);
-        if (PROD) L -= a.prod_ln_sc2;
+        if (SCALED) L -= a.prod_ln_sc2;
       }
     V[0] = L;
   }
@@ -400,7 +404,9 @@ struct SymModHelm {  // COARSE: eps >= 1e-9 Bessel tier (pw_math.cuh k01_asym)
 // so one reciprocal (of 2 W b, which is also the row's factor of the log's product) serves
 // three images: 17 fp64 instructions per row where the image loop needs 22. The same
 // cancellation in b as the Laplace product form, the same per-tile-pair rule (prod_mode).
-template <bool PRESSURE, bool LOWP_, bool CLOG = false, bool PROD_ = false>  // CLOG: coarse table log (eps >= 1e-10)
+// PROD_ = 2 (a period that is not a power of two): unscaled points, A = W + d^2,
+// B = A^2 - 4 d^2 U, sums (B + 2 A W) / (W B) and dX (B + 2 (A - 2 d^2) W) / (W B).
+template <bool PRESSURE, bool LOWP_, bool CLOG = false, int PROD_ = 0>  // CLOG: coarse table log (eps >= 1e-10)
 struct SymStokes {
   static_assert(!PROD_ || (!PRESSURE && LOWP_), "the product form: velocity only, reduced tiers");
   // Without pressure the tile carries (a, Txy, b) with a = L/2 - Txx, b = L/2 - Tyy and
@@ -412,7 +418,8 @@ struct SymStokes {
                                                                                                 : PWB_SYM_STOKES_TPT,
                        CHUNK = 32 / CPT, MINB = PWB_SYM_STOKES_MINB, UNROLL = PWB_SYM_STOKES_UNROLL,
                        LOG_REPL = pwk::kLogTabReplicas, LOG_BITS = CLOG ? PWB_SYM_CLOG_TAB : pwk::kLogTabBits;
-  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_, LOG_SEED = false;
+  static constexpr bool FAST = true, LOWP = LOWP_, EXP_TAB = false, CULL = false, PROD = PROD_ != 0,
+                        SCALED = PROD_ == 1, LOG_SEED = false;
   static constexpr int THREADS = 128;
   template <int NROW, class LK, class B>
   __device__ __forceinline__ static void values_prod(double* V, double dx, double dy, const NearArgs& a, const LK& K,
@@ -425,13 +432,24 @@ struct SymStokes {
         const double ry = n == 1 ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta);  // (dy) - shift, shift = (n - 1) eta
         const double ry2 = ry * ry;
         const double W = ry2 + U;
-        const double aa = fma(W, 0.25, 1.0);
-        const double b = fma(aa, aa, -U);
-        const double b2 = b + b;
-        const double Pr = W * b2;  // 2 W b = r0^2 r-^2 r+^2 / 8
-        const double inv = pwk::rcp_tier<LOWP>(Pr);
-        const double S = fma(aa, W, b2) * inv;        // sum_m 1 / r^2
-        const double Rq = fma(aa - 2.0, W, b2) * inv;  // sum_m rx / r^2, over dX
+        double Pr, S, Rq;
+        if constexpr (SCALED) {
+          const double aa = fma(W, 0.25, 1.0);
+          const double b = fma(aa, aa, -U);
+          const double b2 = b + b;
+          Pr = W * b2;  // 2 W b = r0^2 r-^2 r+^2 / 8
+          const double inv = pwk::rcp_tier<LOWP>(Pr);
+          S = fma(aa, W, b2) * inv;         // sum_m 1 / r^2
+          Rq = fma(aa - 2.0, W, b2) * inv;  // sum_m rx / r^2, over dX
+        } else {
+          const double A = W + a.prod_d2;
+          const double B = fma(A, A, -(a.prod_4d2 * U));
+          const double W2 = W + W;
+          Pr = W * B;  // r0^2 r-^2 r+^2
+          const double inv = pwk::rcp_tier<LOWP>(Pr);
+          S = fma(W2, A, B) * inv;
+          Rq = fma(W2, A - 2.0 * a.prod_d2, B) * inv;
+        }
         if (n == 0) {
           P = Pr;
           tyy = ry2 * S;
@@ -442,7 +460,7 @@ struct SymStokes {
           txyq = fma(ry, Rq, txyq);
         }
       }
-      const double L = pwk::log_fast(P, K, bad);  // the table carries ln(512 / sc^18)
+      const double L = pwk::log_fast(P, K, bad);  // SCALED: the table carries ln(512 / sc^18)
       V[0] = fma(0.5, L, tyy - 9.0);  // L/2 - Txx, Txx = 9 - Tyy
       V[1] = dx * txyq;
       V[2] = fma(0.5, L, -tyy);
@@ -455,17 +473,17 @@ struct SymStokes {
     //   Tyy = sum_n ry_n^2 S_n, Txx = images - Tyy (rx^2/r^2 + ry^2/r^2 = 1 per image; no
     //   exact zero on this path), Txy = sum_n ry_n R_n, pressurelet (sum_n R_n, sum_n ry_n S_n):
     // two fp64 instructions per image besides the reciprocal, instead of three.
-    // PROD (scaled points, period 2, rows at -eta, 0, eta in the tile's units): the product
+    // SCALED (scaled points, period 2, rows at -eta, 0, eta in the tile's units): the product
     // is sc^18 P, the table expects P / 512 of it
-    double P = PROD_ ? 0x1p-9 : 1.0, tyy = 0.0, txy = 0.0, px = 0.0, py = 0.0;
+    double P = SCALED ? 0x1p-9 : 1.0, tyy = 0.0, txy = 0.0, px = 0.0, py = 0.0;
 #pragma unroll
     for (int n = 0; n < NROW; ++n) {
-      const double ry = PROD_ ? (n == 1 ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta)) : row_dy<NXI, NROW>(dy, a, n);
+      const double ry = SCALED ? (n == 1 ? dy : dy - (n == 0 ? -a.prod_eta : a.prod_eta)) : row_dy<NXI, NROW>(dy, a, n);
       const double ry2 = ry * ry;
       double S = 0.0, R = 0.0;
 #pragma unroll
       for (int m = 0; m < NXI; ++m) {
-        const double rx = PROD_ ? (m == 1 ? dx : dx - 2.0 * (m - 1)) : img_dx<NXI, NROW, USK>(dx, a, n, m);
+        const double rx = SCALED ? (m == 1 ? dx : dx - 2.0 * (m - 1)) : img_dx<NXI, NROW, USK>(dx, a, n, m);
         const double r2 = fma(rx, rx, ry2);
         P *= r2;
         const double inv = pwk::rcp_tier<LOWP>(r2);
@@ -508,17 +526,17 @@ struct SymStokes {
     double L = 0.0, txx = 0.0, txy = 0.0, tyy = 0.0, px = 0.0, py = 0.0;
     for (int n = 0; n < NROW; ++n)
       for (int m = 0; m < NXI; ++m) {
-        // PROD: scaled points (shifts 2 (m - 1), (n - 1) eta in the tile's units); the tensor
+        // SCALED: scaled points (shifts 2 (m - 1), (n - 1) eta in the tile's units); the tensor
         // terms do not depend on the scale, each image's log carries ln sc^2
-        const double rx = PROD_ ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
-        const double ry = PROD_ ? dy - a.prod_eta * (n - 1) : row_dy<NXI, NROW>(dy, a, n);
+        const double rx = SCALED ? dx - 2.0 * (m - 1) : img_dx<NXI, NROW>(dx, a, n, m);
+        const double ry = SCALED ? dy - a.prod_eta * (n - 1) : row_dy<NXI, NROW>(dy, a, n);
         if (rx == 0.0 && ry == 0.0) {
           if (n * NXI + m != a.id_img) flag = 1;
           continue;
         }
         const double r2 = fma(rx, rx, ry * ry);
         L += pwk::log_r2_safe(rx, ry);
-        if (PROD_) L -= a.prod_ln_sc2;
+        if (SCALED) L -= a.prod_ln_sc2;
         txx += rx * rx / r2;
         txy += rx * ry / r2;
         tyy += ry * ry / r2;
@@ -618,26 +636,26 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
 }
 
 // Product-form tiles (SymLaplace / SymStokes PROD), per tile pair from the row box and the
-// column box (xmin, -xmax, ymin, -ymax; the period is 2 in the tile's units, the image rows
-// sit at (n - 1) eta):
-//   0  some pair may come within a quarter unit (d / 8) of an image of the +2 or the -2
+// column box (xmin, -xmax, ymin, -ymax; `period` is 2 for the scaled tiles and d for the
+// unscaled ones, the image rows sit at (n - 1) eta):
+//   0  some pair may come within period / 8 of an image of the +period or the -period
 //      column in both x and y: the image loop;
 //   1  every pair stays clear of those images: the product form;
 //   2  and no image can coincide with a pair at all (the boxes are apart by more than
 //      2^-100 around every image), so every product is a normal number: the product form
 //      without the exponent check and without the saved row sums of the careful redo.
 template <int NROW>
-__device__ __forceinline__ int prod_mode(const double* tb, const double* sb, double eta) {
+__device__ __forceinline__ int prod_mode(const double* tb, const double* sb, double eta, double period) {
   const double xlo = tb[0] + sb[1], xhi = -tb[1] - sb[0];  // range of t.x - s.x
   const double ylo = tb[2] + sb[3], yhi = -tb[3] - sb[2];
   auto gap = [](double lo, double hi, double c) { return lo > c ? lo - c : (hi < c ? c - hi : 0.0); };
   const double gx0 = gap(xlo, xhi, 0.0);
-  const double gxs = fmin(gap(xlo, xhi, 2.0), gap(xlo, xhi, -2.0));  // to the nearer side column
+  const double gxs = fmin(gap(xlo, xhi, period), gap(xlo, xhi, -period));  // to the nearer side column
   int mode = 2;
 #pragma unroll
   for (int n = 0; n < NROW; ++n) {
     const double gy = gap(ylo, yhi, NROW == 1 ? 0.0 : (n - 1) * eta);
-    if (!(fmax(gxs, gy) >= 0.25)) return 0;
+    if (!(fmax(gxs, gy) >= 0.125 * period)) return 0;
     if (!(fmax(gx0, gy) > 0x1p-100)) mode = 1;
   }
   return mode;
@@ -798,7 +816,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
           for (int c = 0; c < K::NACC; ++c) keepd[k][c] = racc[k][c];
         using BadD = std::conditional_t<kTab, unsigned, int>;
         BadD badd = 0;
-        const bool dprod = K::PROD && prod_mode<NROW>(rb, cbx, a.prod_eta) >= 1;  // block-uniform
+        const bool dprod = K::PROD && prod_mode<NROW>(rb, cbx, a.prod_eta, a.prod_period) >= 1;  // block-uniform
         const size_t l0 = static_cast<size_t>(I) * TILE + tid;
         auto diag_loop = [&](auto prod) {
 #pragma unroll 2
@@ -969,7 +987,7 @@ __device__ __forceinline__ void near_sym_body(const SymArgs& S) {
     using BadT = std::conditional_t<kTab, unsigned, int>;  // see pwk::log_bad
     int pmode = 0;
     if constexpr (K::PROD) {
-      pmode = prod_mode<NROW>(rb, cbx, a.prod_eta);  // block-uniform
+      pmode = prod_mode<NROW>(rb, cbx, a.prod_eta, a.prod_period);  // block-uniform
       // dead rows / columns sit at the origin with weight 0: their products may vanish, so a
       // ragged tile pair keeps the check
       if (pmode == 2 && (static_cast<size_t>(I + 1) * TILE > n || jbase + CT > n)) pmode = 1;

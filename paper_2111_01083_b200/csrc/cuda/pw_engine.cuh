@@ -89,12 +89,15 @@ struct NearArgs {
   double cheb_tol = 0.0;         // screened symmetric tile: per-tile-pair Chebyshev K0 fit (0: off)
   double inv_beta2 = 0.0;
   // Product-form symmetric tiles (near_sym_impl.cuh SymLaplace / SymStokes PROD):
-  // src / tgt hold the binned points times prod_sc = 2 / d, an exact power of two (0: off),
-  // so the period is 2 in the tile's units
+  // src / tgt hold the binned points times prod_sc: 2 / d when that is an exact power of two,
+  // so the period is 2 in the tile's units, else 1 (0: off)
   double prod_sc = 0.0;
   double prod_log_off = 0.0;     // ln(16 / prod_sc^6) (Laplace), ln(512 / prod_sc^18) (Stokeslet): added to the log table's entries
   double prod_ln_sc2 = 0.0;      // ln(prod_sc^2): one image's log offset on the careful path
   double prod_eta = 0.0;         // eta * prod_sc: the image rows' offset in the tile's units (3 x 3 images)
+  int prod = 0;                  // 0: off; 1: points scaled to period 2; 2: unscaled points (prod_sc = 1), any period
+  double prod_period = 2.0;      // the period in the tile's units: 2 (scaled) or d
+  double prod_d2 = 0.0, prod_4d2 = 0.0;  // unscaled form: d^2, 4 d^2
   // host side only: a split one-sided tile may run on its own stream (a parallel branch of a
   // captured small call, engine.cu total_eager); the partials' reduction waits for tile_done
   void* tile_stream = nullptr;
@@ -144,7 +147,7 @@ void launch_fx_finish(const unsigned long long* fx, size_t n, double* out0, int 
                       const int* out_row, const unsigned* maxhi_dev, size_t n_src, int k_host, const int* flag,
                       cudaStream_t st);
 // host-only: number of work items of the symmetric decomposition (0 if none)
-// (prod: the product-form Laplace tile, NearArgs::prod_sc != 0)
+// (prod: a product-form tile runs, NearArgs::prod != 0)
 long near_sym_item_count(NearKind kind, size_t n, bool prod = false);
 // Tile size (points) and column tiles per work item of the symmetric tile of `kind`.
 void near_sym_shape(NearKind kind, int* tile, int* chunk);

@@ -238,11 +238,15 @@ def test_item_counts_match_the_device_decomposition(pw):
         assert nout == 1
         if want is not None:
             assert items == want
-    # a period that is not a power of two keeps the image-loop tile's decomposition
+    # any period takes the product-form tile's decomposition (unscaled form when d is not a power of two)
     pz15 = pw.make_periodizer(pw.Pde.Poisson, 0.0, pw.make_unit_cell(1.5, 0.0, 1.0, pw.Periodicity.Singly), 1e-10)
     n = 1000000
+    nb, ncb = (n + 1023) // 1024, (n + 255) // 256
+    assert pw.near_sym_items(pz15, n)[0] == sum((ncb - 4 * i + 3) // 4 for i in range(nb))
+    # the full precision tier (eps < 1e-11) keeps the image-loop tile
+    pzf = pw.make_periodizer(pw.Pde.Poisson, 0.0, cell, 1e-12)
     nb, ncb = (n + 511) // 512, (n + 127) // 128
-    assert pw.near_sym_items(pz15, n)[0] == sum((ncb - 4 * i + 31) // 32 for i in range(nb))
+    assert pw.near_sym_items(pzf, n)[0] == sum((ncb - 4 * i + 31) // 32 for i in range(nb))
     st = pw.make_periodizer(pw.Pde.Stokes, 0.0, pw.make_unit_cell(1.0, 0.0, 1.0), 1e-8)
     assert pw.near_sym_items(st, 300, pw.ApplyOptions(with_pressure=True))[1] == 3
 

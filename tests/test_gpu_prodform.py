@@ -26,7 +26,7 @@ def _points(rng, d, n):
 
 
 @pytest.mark.parametrize("eps", [1e-10, 1e-11])
-@pytest.mark.parametrize("d", [1.0, 0.5, 4.0])
+@pytest.mark.parametrize("d", [1.0, 0.5, 4.0, 1.5, 0.3])  # powers of two: scaled points; the others: unscaled form
 def test_product_form_matches_image_loop(pw, gpu, ref, monkeypatch, d, eps):
     rng = np.random.default_rng(int(d * 8) + 3)
     n = 40000
@@ -59,20 +59,21 @@ def test_product_form_matches_image_loop(pw, gpu, ref, monkeypatch, d, eps):
     assert rel_l2(prod[idx], want) <= 1e-11
 
 
-def test_product_form_needs_power_of_two_period(pw, gpu, monkeypatch):
-    """d = 1.5: scaling by 2 / d would round the points, so the image loop runs (bitwise the
-    PWB_NO_PROD result)."""
+def test_product_form_unscaled_at_a_power_of_two(pw, gpu, monkeypatch):
+    """PWB_PROD_UNSCALED=1 runs the any-period form at d = 1: the same field as the scaled
+    form to the tier's accuracy."""
     rng = np.random.default_rng(5)
     n = 36000
-    src = _points(rng, 1.5, n)
+    src = _points(rng, 1.0, n)
     q = rng.standard_normal(n)
     q -= q.mean()
-    pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, pw.make_unit_cell(1.5, 0.0, 1.0, pw.Periodicity.Singly), 1e-10)
+    pz = pw.make_periodizer(pw.Pde.Poisson, 0.0, pw.make_unit_cell(1.0, 0.0, 1.0, pw.Periodicity.Singly), 1e-10)
     sys_ = pw.ParticleSystem(sources=src, targets=src, charges=q)
     a = pw.near_field(pz, sys_).scalar
-    monkeypatch.setenv("PWB_NO_PROD", "1")
+    monkeypatch.setenv("PWB_PROD_UNSCALED", "1")
     b = pw.near_field(pz, sys_).scalar
-    assert np.array_equal(a, b)
+    assert not np.array_equal(a, b)
+    assert rel_l2(a, b) <= 2e-12
 
 
 def test_product_form_duplicates_and_image_coincidence(pw, gpu):
@@ -130,7 +131,7 @@ def _points2(rng, d, eta, n):
 
 
 @pytest.mark.parametrize("eps", [1e-8, 1e-11])
-@pytest.mark.parametrize("d,eta", [(1.0, 1.0), (2.0, 0.7), (0.5, 0.4)])
+@pytest.mark.parametrize("d,eta", [(1.0, 1.0), (2.0, 0.7), (0.5, 0.4), (1.5, 1.0), (3.0, 2.9)])
 def test_stokeslet_product_form_matches_image_loop(pw, gpu, ref, monkeypatch, d, eta, eps):
     rng = np.random.default_rng(int(d * 8) + 11)
     n = 36000
@@ -163,11 +164,11 @@ def test_stokeslet_product_form_matches_image_loop(pw, gpu, ref, monkeypatch, d,
 
 
 def test_stokeslet_product_form_excluded_cases(pw, gpu, monkeypatch):
-    """A skewed cell, a period that is not a power of two and the pressure output keep the
-    image loop (bitwise the PWB_NO_PROD result)."""
+    """A skewed cell and the pressure output keep the image loop (bitwise the PWB_NO_PROD
+    result)."""
     rng = np.random.default_rng(31)
     n = 34000
-    for d, xi, eta, pressure in [(1.0, 0.25, 0.9, False), (1.5, 0.0, 1.0, False), (1.0, 0.0, 1.0, True)]:
+    for d, xi, eta, pressure in [(1.0, 0.25, 0.9, False), (1.0, 0.0, 1.0, True)]:
         cell = pw.make_unit_cell(d, xi, eta)
         src = np.column_stack([rng.uniform(-0.5, 0.5, n), rng.uniform(-0.5, 0.5, n)]) @ np.array([[d, 0.0], [xi, eta]])
         src = np.ascontiguousarray(src)
@@ -207,7 +208,7 @@ def test_stokeslet_product_form_duplicates_and_image_coincidence(pw, gpu):
 
 # ------------------------------------------------------------------ Laplace, 3 x 3 images
 @pytest.mark.parametrize("eps", [1e-10, 1e-11])
-@pytest.mark.parametrize("d,eta", [(1.0, 1.0), (2.0, 0.7), (0.5, 0.4)])
+@pytest.mark.parametrize("d,eta", [(1.0, 1.0), (2.0, 0.7), (0.5, 0.4), (1.5, 1.0)])
 def test_laplace_3x3_product_form_matches_image_loop(pw, gpu, ref, monkeypatch, d, eta, eps):
     """Unskewed doubly periodic Poisson above the symmetric threshold: every image row in
     closed form."""
