@@ -1122,7 +1122,11 @@ bool prod_eligible(const periwave::Periodizer& pz, NearKind nk, size_t n) {
   if (c.periodicity == periwave::Periodicity::Doubly && (c.xi != 0.0 || c.m0 != 1)) return false;
   if (n < 4096 || !(pz.eps >= 1e-11) || std::getenv("PWB_FULL_PRECISION") != nullptr) return false;
   if (std::getenv("PWB_NO_PROD") != nullptr || std::getenv("PWB_NO_BINNING") != nullptr) return false;
-  return c.d > 0.0 && c.d >= 0x1p-400 && c.d <= 0x1p400;
+  // scaled form (d a power of two): any representable scale; unscaled form: products of up
+  // to nine r^2 ~ d^18 must stay normal numbers
+  int e = 0;
+  if (c.d > 0.0 && std::frexp(c.d, &e) == 0.5) return e >= -400 && e <= 400;
+  return c.d >= 0x1p-30 && c.d <= 0x1p30;
 }
 // Sets the tile's constants when eligible; the caller bins (bin_inputs scales the gathered
 // points). A period that is a power of two lets the points be scaled by 2 / d exactly (the

@@ -642,7 +642,8 @@ __device__ __forceinline__ unsigned image_mask(const double* rb, const double* c
 //      column in both x and y: the image loop;
 //   1  every pair stays clear of those images: the product form;
 //   2  and no image can coincide with a pair at all (the boxes are apart by more than
-//      2^-100 around every image), so every product is a normal number: the product form
+//      2^-40 periods around every image), so every product -- down to 2^-276 d^18 for nine
+//      images, d within 2^+-30 in the unscaled form -- is a normal number: the product form
 //      without the exponent check and without the saved row sums of the careful redo.
 template <int NROW>
 __device__ __forceinline__ int prod_mode(const double* tb, const double* sb, double eta, double period) {
@@ -656,7 +657,7 @@ __device__ __forceinline__ int prod_mode(const double* tb, const double* sb, dou
   for (int n = 0; n < NROW; ++n) {
     const double gy = gap(ylo, yhi, NROW == 1 ? 0.0 : (n - 1) * eta);
     if (!(fmax(gxs, gy) >= 0.125 * period)) return 0;
-    if (!(fmax(gx0, gy) > 0x1p-100)) mode = 1;
+    if (!(fmax(gx0, gy) > 0x1p-40 * period)) mode = 1;
   }
   return mode;
 }
