@@ -26,13 +26,13 @@
 #include "near_common.cuh"
 
 #ifndef PWB_MH_SRC_UNROLL
-#define PWB_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c2: 2 -> 579 ms, 4 -> 566)
+#define PWB_MH_SRC_UNROLL 8  // sources per unrolled step of the screened image-outer sweeps (c2: 2 -> 579 ms, 4 -> 566; r3u/r3v with today's tile: 4 -> 488, 8 -> 467, 12 -> 458, 16 -> 460; with the near sweep 6 / 8 / 12 -> 460 / 455 / 456)
 #endif
 #ifndef PWB_MH_GEN_UNROLL
 #define PWB_MH_GEN_UNROLL 1  // sources per unrolled step of the per-pair-dispatch sweep
 #endif
 #ifndef PWB_MH_NEAR_SWEEP
-#define PWB_MH_NEAR_SWEEP 0  // 1: a tile pair wholly in 2 <= x < 6 gets its own sweep (c2: 520 ms vs 512 without: smaller code wins)
+#define PWB_MH_NEAR_SWEEP 1  // 1: a tile pair wholly in 2 <= x < 6 gets its own sweep (round 1, unroll 4: 520 ms vs 512 without; r3v at unroll 8: 455 vs 467)
 #endif
 #ifndef PWB_MH_TPT
 #define PWB_MH_TPT 1  // targets per thread of the screened one-sided tiles

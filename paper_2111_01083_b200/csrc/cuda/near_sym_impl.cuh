@@ -57,7 +57,7 @@ namespace sym {
 #define PWB_SYM_MH_UNROLL_M 3  // image columns per unrolled step of the screened symmetric tile (c5 slice: 1 -> 573 ms, 3 -> 480)
 #endif
 #ifndef PWB_SYM_MH_SRC_UNROLL
-#define PWB_SYM_MH_SRC_UNROLL 4  // sources per unrolled step of the screened image-outer sweeps (c5 slice: 2 -> 159 ms, 4 -> 154)
+#define PWB_SYM_MH_SRC_UNROLL 8  // sources per unrolled step of the screened image-outer sweeps (c5 slice: 2 -> 159 ms, 4 -> 154; c5 full, r3x: 2 -> 138.9 s, 4 -> 132.1, 6 -> 127.9, 8 -> 127.1)
 #endif
 #ifndef PWB_SYM_MH_GEN_UNROLL
 #define PWB_SYM_MH_GEN_UNROLL 1  // sources per unrolled step of the per-pair-dispatch sweep (c5 slice: 4 -> 153.6 ms, 1 -> 143.7)
