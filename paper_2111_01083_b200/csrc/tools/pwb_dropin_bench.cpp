@@ -94,7 +94,76 @@ int cache_check() {
   return mismatches ? 1 : 0;
 }
 
+// --error-check: the drop-in total_field / apply_far leave the point checks to the device
+// (api.cu validated_device_call); the error a caller sees must still be the one the
+// reference raises first (validate_system before every other check, apply.cpp:417-430,
+// cell.cpp:77-94). Prints one JSON line; exit 1 when a case raises something else.
+int error_check() {
+  using periwave::ErrorCode;
+  periwave::Rng rng(5);
+  const size_t n = 400;
+  periwave::ParticleSystem good;
+  good.sources.resize(n);
+  good.charges.resize(n);
+  double mean = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    good.sources[i] = {rng.uniform() - 0.5, rng.uniform() - 0.5};
+    mean += (good.charges[i] = rng.uniform() - 0.5);
+  }
+  for (auto& q : good.charges) q -= mean / n;
+  good.targets = good.sources;
+  const periwave::Periodizer pz = periwave::make_periodizer(
+      periwave::Pde::Poisson, 0.0, periwave::make_unit_cell(1.0, 0.0, 1.0, periwave::Periodicity::Doubly), 1e-8);
+  int failures = 0, cases = 0;
+  std::string report;
+  auto expect = [&](const char* name, const periwave::ParticleSystem& sys, int want, bool far_only) {
+    int got = -1;  // -1: no error
+    try {
+      if (far_only)
+        periwave::apply_far(pz, sys);
+      else
+        periwave::total_field(pz, sys);
+    } catch (const periwave::Error& e) {
+      got = static_cast<int>(e.code());
+    }
+    ++cases;
+    if (got != want) ++failures;
+    report += std::string(report.empty() ? "" : ", ") + "\"" + name + "\": " + std::to_string(got);
+  };
+  for (bool far_only : {false, true}) {
+    const std::string tag = far_only ? "far_" : "";
+    expect((tag + "ok").c_str(), good, -1, far_only);
+    periwave::ParticleSystem s = good;
+    s.sources[7].x = 0.75;  // outside the cell
+    expect((tag + "outside_source").c_str(), s, static_cast<int>(ErrorCode::OutOfInterval), far_only);
+    s = good;
+    s.targets[9].y = -0.9;
+    expect((tag + "outside_target").c_str(), s, static_cast<int>(ErrorCode::OutOfInterval), far_only);
+    s = good;
+    s.charges.pop_back();
+    expect((tag + "short_charges").c_str(), s, static_cast<int>(ErrorCode::LengthMismatch), far_only);
+    s.sources[3].x = 2.0;  // points are checked before lengths
+    expect((tag + "outside_and_short").c_str(), s, static_cast<int>(ErrorCode::OutOfInterval), far_only);
+    s = good;
+    s.charges[0] += 1.0;
+    expect((tag + "not_neutral").c_str(), s, static_cast<int>(ErrorCode::NotNeutral), far_only);
+    s.targets[1].x = -3.0;  // ... and before neutrality
+    expect((tag + "outside_and_not_neutral").c_str(), s, static_cast<int>(ErrorCode::OutOfInterval), far_only);
+  }
+  std::printf("{\"error_check\": true, \"cases\": %d, \"failures\": %d, \"codes\": {%s}}\n", cases, failures,
+              report.c_str());
+  return failures ? 1 : 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 2 && std::string(argv[1]) == "--error-check") {
+    try {
+      return error_check();
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "error: %s\n", e.what());
+      return 1;
+    }
+  }
   if (argc == 2 && std::string(argv[1]) == "--cache-check") {
     try {
       return cache_check();

@@ -73,3 +73,13 @@ def test_plan_cache_under_eviction(gpu):
     assert r.returncode == 0, r.stdout + r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["mismatches"] == 0 and line["calls"] == 36
+
+
+def test_dropin_errors_follow_the_reference_precedence(gpu):
+    """The drop-in total_field / apply_far validate points on the device; the error raised
+    is still the reference's first one (validate_system before lengths' consumers,
+    neutrality and everything else, apply.cpp:417-430)."""
+    r = subprocess.run([BIN, "--error-check"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["failures"] == 0 and line["cases"] == 14, line
